@@ -1,0 +1,24 @@
+"""fp64 CPU oracle for SPAgent's shared-prefix paged GQA decode-attention step.
+
+TEST INFRASTRUCTURE ONLY.  Only `tests/`, `__graft_entry__.smoke()` and `bench.py`'s
+`cpu_baseline` leg (and its `--impl reference` arm) may import, call or execute
+anything in this package.  The product path (`paper_2511_20048_b200`) never imports it
+and shares no code, header, table or helper with it; the two meet only through the
+seeded input generators in `spa_inputs`, which hold none of the method's arithmetic.
+
+Contents
+  attention.py  decode attention, written as its plain definition (softmax(scale q K^T) V
+                per query head, GQA head mapping, optional sliding window), and the
+                split-KV log-sum-exp merge.
+  kvmodel.py    a dense logical KV model (a fork is a physical copy) plus an independent
+                model of the documented paging policy (lowest-free page id, refcounts,
+                copy-on-write of the partial last page).
+
+Where the paper is silent (it never mentions attention, KV caches or pages -- see
+SURVEY.md Sec. 0.1) the readings used here are listed in DESIGN.md Sec. 3 and cited
+by number ("reading #k") in the docstrings.
+
+Parity status: every function here is pinned by `tests/test_oracle_*.py` against
+closed forms, brute force, a library routine (torch SDPA in fp64) or hand-derived
+golden fixtures (`tests/golden/`); none is "parity unpinned".
+"""

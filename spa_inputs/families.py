@@ -1,0 +1,186 @@
+"""Discriminating input families for parity, as bf16 bit patterns.
+
+With q, k ~ N(0,1) and scale 1/sqrt(d) the softmax over thousands of keys is almost flat,
+so |O| ~ 0.01-0.03 and a 2e-2 max-abs gate would pass a kernel that drops or
+mis-indexes pages.  These families make wrong gathers move O by O(1):
+
+  flat       counter-hash values (spa_inputs.kv_bits_np) for q, k, v
+  peaky      flat, with q multiplied by 4 (exact: exponent + 2) -> logit std ~ 5
+  needle_*   one key per (group|member, KV head) is 2^a * qbase, where every query row
+             of that group/member and KV head is qbase + e/32, e in {-1, 0, 1}; `a` is
+             the smallest exponent for which a Cauchy-Schwarz bound guarantees the needle
+             beats every other logit by ln(n) + 8 -> needle weight >= 1 - e^-8.
+               needle_shared: needle inside the shared prefix c_i
+               needle_tail:   one needle per member, inside the member's private tail
+               needle_cow:    needle inside the copied partial page [16 floor(P/16), P)
+  *_pos      V is position-coded: v[j, g, c] = ((37 j + 11 c + 5 g + 3 o) mod 127 - 63)/32
+             (o = origin stream id), so O ~ v[j*] identifies the gathered position.
+
+Every value is an integer multiple of 2^-5 (times a power of two) with |mantissa| < 2^8,
+hence exact in bf16; no rounding happens anywhere in input construction.  Needle
+amplitudes use only vector norms (no attention arithmetic).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import KIND_K, KIND_Q, KIND_V, MASK32, _combine, hash32, kv_bits_np
+from .workloads import Recipe, call_log
+
+FAMILIES = ("flat", "peaky", "needle_shared_pos", "needle_tail_pos", "needle_cow_pos", "flat_pos")
+
+
+def origin_id(name) -> int:
+    gi, who = name
+    return gi * 64 + (0 if who == "main" else 1 + int(who[1:]))
+
+
+def _bits_to_f32(bits):
+    return (bits.astype(np.uint32) << 16).view(np.float32)
+
+
+def _f32_to_bits(f):
+    u = np.asarray(f, np.float32).view(np.uint32)
+    assert not np.any(u & 0xFFFF), "inexact bf16 input"
+    return (u >> 16).astype(np.uint16)
+
+
+def _small_ints(seed, salt, shape, lo, hi):
+    """Deterministic integers in [lo, hi] from the counter hash."""
+    n = int(np.prod(shape))
+    h = hash32((np.arange(n, dtype=np.int64) * 0x85EBCA6B + _combine(np.int64(seed & MASK32), np.int64(salt))) & MASK32)
+    return (lo + (h % (hi - lo + 1))).reshape(shape)
+
+
+def _poscode_v(origin, positions, n_heads, head_dim):
+    j = np.asarray(positions, np.int64)[:, None, None]
+    g = np.arange(n_heads, dtype=np.int64)[None, :, None]
+    c = np.arange(head_dim, dtype=np.int64)[None, None, :]
+    s = (37 * j + 11 * c + 5 * g + 3 * origin) % 127 - 63
+    return _f32_to_bits(s.astype(np.float32) / 32.0)
+
+
+@dataclass
+class BatchInputs:
+    recipe: Recipe
+    family: str
+    layers: list            # model layer indices the arrays below cover
+    ops: list               # call_log ops
+    batch: list             # request names of the decode batch
+    append_k: dict          # op index -> [L, n, Hkv, d] uint16
+    append_v: dict
+    q: np.ndarray           # [L, N, Hq, d] uint16
+    needles: dict           # (name|group, kv head) -> logical position (diagnostic)
+
+
+def make_inputs(recipe: Recipe, family: str = "flat", layers=None, step: int = 0) -> BatchInputs:
+    m = recipe.model
+    Hq, Hkv, d = m.num_q_heads, m.num_kv_heads, m.head_dim
+    G = Hq // Hkv
+    layers = list(range(m.num_layers)) if layers is None else list(layers)
+    L = len(layers)
+    ops, batch = call_log(recipe)
+    seed = recipe.seed
+    N = len(batch)
+    q = kv_bits_np(seed, KIND_Q, 1_000_000 + step, layers, np.arange(N), Hq, d)  # [L, N, Hq, d]
+    if family.startswith("peaky"):
+        q = _f32_to_bits(_bits_to_f32(q) * 4.0)
+
+    needle_mode = None
+    for mode in ("needle_shared", "needle_tail", "needle_cow"):
+        if family.startswith(mode):
+            needle_mode = mode
+    pos_v = family.endswith("_pos")
+
+    # ---- needle placement: which (stream origin, position, kv head) gets which base vector
+    placements = {}   # (origin_name, position) -> list of (kv_head, base_key)
+    needles = {}
+    bases = {}        # base_key -> qbase bits [L, Hkv, d]
+    if needle_mode is not None:
+        batch_idx = {nm: i for i, nm in enumerate(batch)}
+        for gi, g in enumerate(recipe.groups):
+            members = []
+            if g.parent_tail is not None:
+                members.append(((gi, "main"), g.parent_tail))
+            members += [((gi, f"f{j}"), t) for j, t in enumerate(g.fork_tails)]
+            if needle_mode == "needle_shared" or (needle_mode == "needle_cow" and g.prefix % 16 == 0):
+                base_key = ("group", gi)
+                pos = int(_small_ints(seed, 11 + gi, (1,), 0, g.prefix - 1)[0])
+                placements.setdefault(((gi, "main"), pos), []).append(base_key)
+                needles[base_key] = pos
+                for nm, _ in members:
+                    bases.setdefault(base_key, []).append(batch_idx[nm])
+            elif needle_mode == "needle_cow":
+                base_key = ("group", gi)
+                lo = (g.prefix // 16) * 16
+                pos = int(_small_ints(seed, 17 + gi, (1,), lo, g.prefix - 1)[0])
+                placements.setdefault(((gi, "main"), pos), []).append(base_key)
+                needles[base_key] = pos
+                for nm, _ in members:
+                    bases.setdefault(base_key, []).append(batch_idx[nm])
+            else:  # needle_tail
+                for nm, tail in members:
+                    if tail <= 0:
+                        continue
+                    base_key = ("member", nm)
+                    pos = g.prefix + int(_small_ints(seed, 23 + origin_id(nm), (1,), 0, tail - 1)[0])
+                    placements.setdefault((nm, pos), []).append(base_key)
+                    needles[base_key] = pos
+                    bases.setdefault(base_key, []).append(batch_idx[nm])
+
+    # rewrite the query rows that follow a needle base: q = qbase + e/32
+    base_vecs = {}
+    qf = _bits_to_f32(q).copy()
+    for bi, (base_key, rows) in enumerate(bases.items()):
+        b = kv_bits_np(seed, KIND_Q, 2_000_000 + bi, layers, np.arange(1), Hkv, d)[:, 0]  # [L, Hkv, d]
+        base_vecs[base_key] = _bits_to_f32(b)
+        for r in rows:
+            e = _small_ints(seed, 3_000_000 + bi * 1024 + r, (L, Hq, d), -1, 1).astype(np.float32) / 32.0
+            for h in range(Hq):
+                qf[:, r, h, :] = base_vecs[base_key][:, h // G, :] + e[:, h, :]
+    q = _f32_to_bits(qf)
+
+    # needle amplitude 2^a from norms only (Cauchy-Schwarz): for every row
+    #   scale * 2^a * (q_i . b) - scale * |q_i| * max_j |k_j| >= ln(n) + 8
+    n_max = max(g.prefix + max([g.parent_tail or 0] + list(g.fork_tails)) for g in recipe.groups)
+    kmax = 3.9375 * np.sqrt(d)   # |k_j| <= max|entry| * sqrt(d) for counter-hash keys
+    amp = {}
+    for base_key, rows in bases.items():
+        bv = base_vecs[base_key]
+        need = 0
+        for r in rows:
+            for h in range(Hq):
+                qi = qf[:, r, h, :]
+                bb = bv[:, h // G, :]
+                dot = (qi.astype(np.float64) * bb).sum(-1).min()
+                nq = np.sqrt((qi.astype(np.float64) ** 2).sum(-1)).max()
+                target = (np.log(n_max) + 8) / m.softmax_scale + nq * kmax
+                a = 0
+                while (2.0 ** a) * dot < target and a < 12:
+                    a += 1
+                need = max(need, a)
+        amp[base_key] = need
+
+    append_k, append_v = {}, {}
+    for oi, op in enumerate(ops):
+        if op[0] != "append":
+            continue
+        _, name, origin, start, n = op
+        pos = np.arange(start, start + n)
+        o = origin_id(origin)
+        k = kv_bits_np(seed, KIND_K, o, layers, pos, Hkv, d)
+        if pos_v:
+            v = np.broadcast_to(_poscode_v(o, pos, Hkv, d)[None], (L, n, Hkv, d)).copy()
+        else:
+            v = kv_bits_np(seed, KIND_V, o, layers, pos, Hkv, d)
+        for (nm, p), keys in placements.items():
+            if nm == origin and start <= p < start + n:
+                kf = _bits_to_f32(k[:, p - start]).copy()   # [L, Hkv, d]
+                for base_key in keys:
+                    kf[:, :, :] = base_vecs[base_key] * (2.0 ** amp[base_key])
+                k[:, p - start] = _f32_to_bits(kf)
+        append_k[oi] = k
+        append_v[oi] = v
+    return BatchInputs(recipe, family, layers, ops, batch, append_k, append_v, q, needles)
