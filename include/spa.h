@@ -1,0 +1,206 @@
+/*
+ * spa.h -- C ABI of the shared-prefix paged GQA decode-attention step under SPAgent's
+ * action speculation (arXiv 2511.20048), B200 / sm_100a.
+ *
+ * What the calls compute, and where it is defined
+ * ------------------------------------------------
+ * SPAgent runs k short speculative requests beside each agent's main reasoning request
+ * (Sec. III-B/C), so one engine decode iteration serves
+ * N = N_m + N_s + N_a requests (Table I) and costs T_h(emptyset, N)
+ * (Eq. 3).  Every speculative sample is drawn from the agent context
+ * c_i ("all samples of one request share the same prefix"; c_i defined at
+ * PAPER.md:135).  This library is the attention part of that decode iteration: paged
+ * KV, copy-free forks of c_i, and per-layer decode attention that reads each shared
+ * prefix page ONCE per (KV head, request group).  The paper itself never writes
+ * attention down; the readings used for everything it leaves open are numbered in
+ * DESIGN.md Sec. 3 ("reading #k").
+ *
+ * Conventions
+ *  - All device memory named in these signatures is caller-owned (PyTorch allocates it)
+ *    unless stated otherwise; the library owns host metadata (request table, page
+ *    tables, refcounts, free set, plans) and a plan's own small device buffers.
+ *  - bf16 means IEEE bfloat16 bit patterns (uint16).  Strides are in ELEMENTS.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Device work is
+ *    stream-ordered; host metadata changes take effect when the call returns.
+ *  - Threading: one host thread per pool (the caller serialises calls on a pool and on
+ *    its plans).  spa_last_error() is thread-local.
+ *  - Every call returns a spa_status; no exception ever crosses the ABI.  Host metadata
+ *    mutations are all-or-nothing: on any error nothing observable changed.
+ *  - Asynchronous kernel faults surface as SPA_ERR_CUDA on a later call.
+ */
+#ifndef SPA_H_
+#define SPA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPA_ABI_VERSION 1
+
+typedef enum spa_status {
+    SPA_OK = 0,
+    SPA_ERR_INVALID_ARG = 1,   /* bad shape/argument, duplicate request in a batch, prefix_len > length, empty request in a decode batch */
+    SPA_ERR_NO_PAGES = 2,      /* the pool has too few free pages; nothing was changed */
+    SPA_ERR_BAD_REQUEST = 3,   /* unknown or already-freed request id */
+    SPA_ERR_CUDA = 4,          /* a CUDA runtime/driver call or kernel failed (see spa_last_error) */
+    SPA_ERR_NCCL = 5,          /* NCCL could not be loaded or a collective failed */
+    SPA_ERR_UNSUPPORTED = 6,   /* configuration the kernels do not implement (head_dim, page_size, ...) */
+    SPA_ERR_NO_DEVICE = 7      /* device work requested from a metadata-only pool */
+} spa_status;
+
+typedef int64_t spa_req;                 /* request id: 1, 2, 3, ... never reused (reading #4) */
+typedef struct spa_pool spa_pool;
+typedef struct spa_plan spa_plan;
+typedef struct spa_comm spa_comm;
+
+/* ---------------------------------------------------------------------------------
+ * Paged KV pool
+ * --------------------------------------------------------------------------------- */
+typedef struct spa_pool_config {
+    int32_t num_layers;     /* L                                                       */
+    int32_t num_q_heads;    /* Hq held by this process (its shard when head-sharded)   */
+    int32_t num_kv_heads;   /* Hkv held by this process; Hq % Hkv == 0, G = Hq / Hkv   */
+    int32_t head_dim;       /* d: 64 or 128                                            */
+    int32_t page_size;      /* tokens per page; the decode kernels require 16          */
+    int32_t num_pages;      /* pages in the pool                                       */
+} spa_pool_config;
+
+/* Create a pool over caller-owned device memory.
+ *   k_pool, v_pool: device, bf16 [L][num_pages][Hkv][page_size][d] each, 128-B aligned;
+ *                   the SAME page id is used in every layer.  The library zero-fills
+ *                   both at creation, so never-written slots of a page hold finite
+ *                   values (masked keys are then multiplied by an exact 0).
+ *   k_pool = v_pool = NULL creates a METADATA-ONLY pool: every host-side rule below
+ *   applies, device work is skipped (used by CPU tests of the allocator and planner).
+ * Errors: INVALID_ARG (non-positive sizes, Hq % Hkv), UNSUPPORTED (d not 64/128 or
+ * page_size != 16 with device memory), CUDA. */
+spa_status spa_pool_create(const spa_pool_config* cfg, void* k_pool, void* v_pool, spa_pool** out);
+spa_status spa_pool_destroy(spa_pool* pool);
+
+/* a1: a new, empty request (length 0, no pages). */
+spa_status spa_kv_alloc(spa_pool* pool, spa_req* out_req);
+
+/* a2: append n_new[i] tokens to reqs[i], i < n_req, for ALL layers at once.
+ *   reqs, n_new: host arrays.  A request may appear at most once (INVALID_ARG).
+ *   k_new, v_new: device bf16 [L][T][Hkv][d], T = sum(n_new), tokens ordered request
+ *   by request (in reqs order) then by position.  Paging policy (reading #4): request
+ *   by request, token by token, a page is taken (lowest free id) exactly when
+ *   length % page_size == 0.  If the pages needed exceed the free pages: NO_PAGES and
+ *   nothing changes.  The query of a decode step attends to the key appended here
+ *   (append-then-attend, reading #8). */
+spa_status spa_kv_append(spa_pool* pool, int32_t n_req, const spa_req* reqs, const int32_t* n_new,
+                         const void* k_new, const void* v_new, void* stream);
+
+/* a3: copy-free fork of the first prefix_len tokens of `parent` (the k
+ * speculative samples of PAPER.md:189/:198 reading context c_i).  The child shares
+ * parent pages [0, prefix_len / page_size) (refcount + 1); if prefix_len % page_size
+ * != 0 one fresh page receives a device copy of the parent's partial page, slots
+ * [0, prefix_len % page_size), all layers (copy-on-write at fork time, reading #3).
+ * 0 <= prefix_len <= length(parent), else INVALID_ARG. */
+spa_status spa_fork_request(spa_pool* pool, spa_req parent, int32_t prefix_len, spa_req* out_child,
+                            void* stream);
+
+/* a8: release a request: refcount - 1 on each of its pages; pages reaching 0 return to
+ * the free set.  The id is retired (later use: BAD_REQUEST). */
+spa_status spa_kv_free(spa_pool* pool, spa_req req);
+
+/* Inspection (bit-exact tests).  out_pages receives min(cap, n_pages) page ids. */
+spa_status spa_kv_page_table(const spa_pool* pool, spa_req req, int32_t* out_pages, int32_t cap,
+                             int32_t* out_n_pages, int32_t* out_len);
+/* out_refcount: host int32[num_pages]. */
+spa_status spa_pool_refcounts(const spa_pool* pool, int32_t* out_refcount);
+/* Free page ids in increasing order; out_pages receives min(cap, n) of them. */
+spa_status spa_pool_free_pages(const spa_pool* pool, int32_t* out_pages, int32_t cap, int32_t* out_n);
+
+/* ---------------------------------------------------------------------------------
+ * Step plan (a4): built once per decode step on the host, uploaded once, reused by
+ * every layer.  Groups are requests with the same first page; their shared region is
+ * the longest common page-id prefix (reading #18).  Work items are
+ * (KV head, group-split) and (KV head, member-tail-split); each shared page is read once
+ * per (KV head, group) by one CTA-team holding all R = members x G query rows.
+ * --------------------------------------------------------------------------------- */
+typedef struct spa_plan_config {
+    int32_t sharing;        /* 1: group by shared prefix (default); 0: every request alone (control) */
+    int32_t max_rows;       /* 16 or 32: query rows (members x G) per work item; larger groups
+                               are cut into sub-groups.  0 = 16                                 */
+    int32_t split_pages;    /* max pages per split; 0 = auto (balance over the persistent grid)  */
+    int32_t num_ctas;       /* persistent grid size; 0 = number of SMs                            */
+} spa_plan_config;
+
+/* cfg may be NULL (defaults).  The plan keeps a pointer to `pool`. */
+spa_status spa_plan_create(spa_pool* pool, const spa_plan_config* cfg, spa_plan** out);
+spa_status spa_plan_destroy(spa_plan* plan);
+
+/* (Re)plan a decode batch: reqs[0..n_req) (host), all of length >= 1, no duplicates.
+ *   window > 0: sliding window, request r attends to keys [max(0, n_r - window), n_r)
+ *   (reading #9); window <= 0: full attention.  Batch row i of q/o/lse below is reqs[i].
+ *   The plan's metadata is uploaded to its device buffers on `stream`; device buffers
+ *   only grow (spa_plan_stats.generation changes when they move, which invalidates CUDA
+ *   graphs captured over this plan). */
+spa_status spa_decode_plan(spa_plan* plan, int32_t n_req, const spa_req* reqs, int32_t window, void* stream);
+
+typedef struct spa_plan_stats {
+    int32_t n_req, n_groups, n_desc, n_items, n_records, n_teams, rows_max, generation;
+    int64_t unique_tokens;    /* sum over work descriptors of key tokens read, per KV head     */
+    int64_t unshared_tokens;  /* sum over requests of attended keys, per KV head (no sharing)  */
+    int64_t pages_read;       /* pages read per KV head (page-granular, incl. partial pages)   */
+} spa_plan_stats;
+spa_status spa_plan_get_stats(const spa_plan* plan, spa_plan_stats* out);
+
+/* a5 (+a6): decode attention of one layer for the planned batch.
+ *   q:   device bf16, row i head h at q[i*q_stride_req + h*q_stride_head + c], c < d
+ *   o:   device bf16, same indexing with o strides (head-major or request-major allowed)
+ *   lse: device fp32 natural-log LSE of the scaled logits (reading #7) at
+ *        lse[i*lse_stride_req + h*lse_stride_head], or NULL
+ *   scale: softmax scale (reading #6; 1/sqrt(d) for Qwen2.5, 168^-1/2 for Gemma-3).
+ * O is rounded to bf16 (RNE) from fp32 (reading #10).  If the plan split any request,
+ * its fp32 partials are merged on the same stream (spa_merge_splits semantics). */
+spa_status spa_decode_attention(const spa_plan* plan, int32_t layer,
+                                const void* q, int64_t q_stride_req, int64_t q_stride_head,
+                                void* o, int64_t o_stride_req, int64_t o_stride_head,
+                                float* lse, int64_t lse_stride_req, int64_t lse_stride_head,
+                                float scale, void* stream);
+
+/* a6: split-KV partial-LSE merge (north_star; oracle/attention.py merge_partials).
+ * For request i < n_req and head h < num_heads, partial records
+ * s in [rec_ptr[i], rec_ptr[i+1]) hold part_o[(s*num_heads + h)*head_dim + c] (fp32) and
+ * part_lse[s*num_heads + h] (natural log; -inf = empty split):
+ *     LSE = m + ln sum_{s live} exp(LSE_s - m),  O = sum_s exp(LSE_s - LSE) O_s
+ * all partials -inf -> O = 0, LSE = -inf.  Requests with an EMPTY record range are not
+ * written (their output was produced directly).  All pointers are device pointers;
+ * rec_ptr is int32[n_req + 1].  o is bf16 (RNE), lse may be NULL. */
+spa_status spa_merge_splits(int32_t n_req, int32_t num_heads, int32_t head_dim, const int32_t* rec_ptr,
+                            const float* part_o, const float* part_lse,
+                            void* o, int64_t o_stride_req, int64_t o_stride_head,
+                            float* lse, int64_t lse_stride_req, int64_t lse_stride_head, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * Multi-GPU: KV-head sharding with an NCCL all-gather of head outputs (a7).
+ * Rank r of n holds KV heads [r Hkv/n, (r+1) Hkv/n) and q heads [r Hq/n, (r+1) Hq/n) in
+ * its own pool (num_kv_heads / num_q_heads of its spa_pool_config are the LOCAL counts).
+ * Every rank replays the same allocator calls, so page tables and plans are identical
+ * without communication.  NCCL (libnccl.so.2) is loaded at spa_comm_create.
+ * --------------------------------------------------------------------------------- */
+spa_status spa_nccl_unique_id(void* out_id /* 128 bytes (ncclUniqueId) */);
+/* Collective over `world` ranks; the calling thread's current CUDA device is used. */
+spa_status spa_comm_create(const void* unique_id, int32_t rank, int32_t world, spa_comm** out);
+spa_status spa_comm_destroy(spa_comm* comm);
+/* Decode this rank's heads straight into its slot of o_gathered, then all-gather in place.
+ *   q_local:     bf16 [N][Hq_local][d] with the given strides
+ *   o_gathered:  bf16 [world][Hq_local][N][d] contiguous (= [Hq][N][d], head-major)
+ *   lse_gathered: fp32 [world][Hq_local][N] or NULL */
+spa_status spa_decode_attention_sharded(const spa_plan* plan, spa_comm* comm, int32_t layer,
+                                        const void* q_local, int64_t q_stride_req, int64_t q_stride_head,
+                                        void* o_gathered, float* lse_gathered, float scale, void* stream);
+
+/* Library info */
+int32_t spa_abi_version(void);
+const char* spa_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPA_H_ */

@@ -1,0 +1,316 @@
+// Step planner: groups, splits, work items, static schedule.
+//
+// A decode batch under SPAgent holds main requests and the k speculative samples forked
+// from each one's context c_i (PAPER.md:189, :198, :292 Table I, :335).  Requests whose
+// page tables start with the same page id form a group; the group's shared region is the
+// longest common page-id prefix of its members (reading #18).  For every KV head:
+//   - one work descriptor per split of the shared region carries ALL R = members x G
+//     query rows, so each shared page is read once per (KV head, group);
+//   - each member's private tail [S, n_m) is its own descriptor (its rows only).
+// Sliding windows (reading #9) restrict every range to the union of the members'
+// windows; per-member lower bounds are applied as masks inside the kernel.
+// Splits are sized so the persistent grid (num_ctas CTAs x teams) is balanced by a
+// longest-processing-time (LPT) static assignment; a request that ends up in more than
+// one descriptor gets fp32 partial records that spa_merge_splits combines.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <numeric>
+#include <queue>
+#include <unordered_map>
+#include <unordered_set>
+
+#include "../../include/spa_debug.h"
+#include "spa_internal.h"
+
+namespace spa {
+
+int plan_upload(spa_plan* P, void* stream);  // kernels.cu
+void plan_release(spa_plan* P);               // kernels.cu
+
+namespace {
+
+struct Range {
+    int kind;                 // 0 shared (group), 1 member tail
+    int group;
+    std::vector<int> members; // batch rows
+    int32_t a, b;             // tokens [a, b)
+    const std::vector<int32_t>* table;
+};
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace
+}  // namespace spa
+
+using namespace spa;
+
+extern "C" {
+
+spa_status spa_plan_create(spa_pool* pool, const spa_plan_config* cfg, spa_plan** out) {
+    if (!pool || !out) return fail(SPA_ERR_INVALID_ARG, "null argument");
+    *out = nullptr;
+    spa_plan_config c{};
+    c.sharing = 1;
+    if (cfg) c = *cfg;
+    if (c.max_rows == 0) c.max_rows = 16;
+    if (c.max_rows != 16 && c.max_rows != 32) return fail(SPA_ERR_UNSUPPORTED, "max_rows must be 16 or 32");
+    if (c.split_pages < 0 || c.num_ctas < 0) return fail(SPA_ERR_INVALID_ARG, "negative plan option");
+    const int G = pool->cfg.num_q_heads / pool->cfg.num_kv_heads;
+    if (G > c.max_rows) return fail(SPA_ERR_UNSUPPORTED, "GQA group size exceeds max_rows");
+    spa_plan* P = new spa_plan();
+    P->pool = pool;
+    P->cfg = c;
+    P->mt = c.max_rows / 16;
+    int ctas = c.num_ctas;
+    if (ctas == 0) ctas = pool->sm_count > 0 ? pool->sm_count : 148;
+    P->num_ctas = ctas;
+    P->n_teams = ctas * (kWarps / P->mt);
+    *out = P;
+    return SPA_OK;
+}
+
+spa_status spa_plan_destroy(spa_plan* plan) {
+    if (!plan) return SPA_OK;
+    plan_release(plan);
+    delete plan;
+    return SPA_OK;
+}
+
+spa_status spa_decode_plan(spa_plan* P, int32_t n_req, const spa_req* reqs, int32_t window, void* stream) {
+    if (!P) return fail(SPA_ERR_INVALID_ARG, "null plan");
+    spa_pool* pool = P->pool;
+    if (n_req < 0 || (n_req > 0 && !reqs)) return fail(SPA_ERR_INVALID_ARG, "bad request list");
+    const int ps = pool->cfg.page_size;
+    const int Hkv = pool->cfg.num_kv_heads;
+    const int G = pool->cfg.num_q_heads / Hkv;
+    std::vector<const Request*> R(n_req);
+    {
+        std::unordered_set<int64_t> seen;
+        for (int i = 0; i < n_req; ++i)
+            if (!seen.insert(reqs[i]).second) return fail(SPA_ERR_INVALID_ARG, "plan: request listed twice");
+        for (int i = 0; i < n_req; ++i) {
+            auto it = pool->reqs.find(reqs[i]);
+            if (it == pool->reqs.end()) return fail(SPA_ERR_BAD_REQUEST, "plan: unknown request " + std::to_string(reqs[i]));
+            if (it->second.len <= 0) return fail(SPA_ERR_INVALID_ARG, "plan: decode over an empty request (reading #11)");
+            R[i] = &it->second;
+        }
+    }
+    std::vector<int32_t> lo(n_req);
+    for (int i = 0; i < n_req; ++i) lo[i] = window > 0 ? std::max<int32_t>(0, R[i]->len - window) : 0;
+
+    // ---- 1. groups (first page id), then sub-groups of at most max_rows / G members
+    std::vector<std::vector<int>> groups;
+    if (P->cfg.sharing) {
+        std::unordered_map<int32_t, int> by_root;
+        for (int i = 0; i < n_req; ++i) {
+            auto ins = by_root.emplace(R[i]->pages[0], int(groups.size()));
+            if (ins.second) groups.emplace_back();
+            groups[ins.first->second].push_back(i);
+        }
+    } else {
+        for (int i = 0; i < n_req; ++i) groups.push_back({i});
+    }
+    const int max_members = std::max(1, P->cfg.max_rows / G);
+
+    // ---- 2. ranges
+    std::vector<Range> ranges;
+    int n_groups = 0;
+    int64_t unique_tokens = 0, unshared_tokens = 0;
+    for (int i = 0; i < n_req; ++i) unshared_tokens += R[i]->len - lo[i];
+    for (const auto& grp : groups) {
+        for (size_t s0 = 0; s0 < grp.size(); s0 += max_members) {
+            std::vector<int> sg(grp.begin() + s0, grp.begin() + std::min(grp.size(), s0 + max_members));
+            const int gid = n_groups++;
+            int32_t cp = 0;
+            if (sg.size() > 1) {
+                const auto& t0 = R[sg[0]]->pages;
+                for (;; ++cp) {
+                    bool ok = true;
+                    for (int m : sg) {
+                        const auto& t = R[m]->pages;
+                        if (int64_t(R[m]->len) < int64_t(cp + 1) * ps || t[cp] != t0[cp]) { ok = false; break; }
+                    }
+                    if (!ok) break;
+                }
+            }
+            const int32_t S = cp * ps;
+            if (S == 0) {
+                for (int m : sg) ranges.push_back(Range{0, gid, {m}, lo[m], R[m]->len, &R[m]->pages});
+                continue;
+            }
+            std::vector<int> shared;
+            int32_t lo_min = S;
+            for (int m : sg)
+                if (lo[m] < S) { shared.push_back(m); lo_min = std::min(lo_min, lo[m]); }
+            if (!shared.empty()) ranges.push_back(Range{0, gid, shared, lo_min, S, &R[sg[0]]->pages});
+            for (int m : sg) {
+                const int32_t a = std::max(S, lo[m]);
+                if (a < R[m]->len) ranges.push_back(Range{1, gid, {m}, a, R[m]->len, &R[m]->pages});
+            }
+        }
+    }
+
+    // ---- 3. split size
+    int64_t total_pages = 0;
+    for (const auto& r : ranges) {
+        unique_tokens += r.b - r.a;
+        total_pages += cdiv(r.b, ps) - r.a / ps;
+    }
+    int32_t C = P->cfg.split_pages;
+    if (C <= 0) {
+        double div = 1.0;
+        if (const char* e = std::getenv("SPA_SPLIT_DIV")) div = std::max(0.25, std::atof(e));
+        const double target = double(total_pages * Hkv) / double(std::max(1, P->n_teams));
+        C = int32_t(std::ceil(target / div));
+        C = std::max(4, std::min(C, 1 << 20));
+    }
+
+    // ---- 4. descriptors, members, pages
+    std::vector<Desc> descs;
+    std::vector<Member> members;
+    std::vector<int32_t> pages;
+    std::vector<int32_t> occ(n_req, 0);
+    int64_t pages_read = 0;
+    for (const auto& r : ranges) {
+        const int32_t pa = r.a / ps, pb = int32_t(cdiv(r.b, ps));
+        for (int32_t s = pa; s < pb; s += C) {
+            const int32_t e = std::min(pb, s + C);
+            Desc d{};
+            d.page_off = int32_t(pages.size());
+            d.n_pages = e - s;
+            d.tok_start = s * ps;
+            d.tok_end = std::min<int32_t>(r.b, e * ps);
+            d.member_off = int32_t(members.size());
+            d.n_members = int32_t(r.members.size());
+            d.kind = r.kind;
+            d.group = r.group;
+            for (int32_t p = s; p < e; ++p) pages.push_back((*r.table)[p]);
+            for (int m : r.members) {
+                members.push_back(Member{m, lo[m], 0, 0});
+                occ[m] += 1;
+            }
+            descs.push_back(d);
+            pages_read += d.n_pages;
+        }
+    }
+    std::vector<int32_t> rec_ptr(n_req + 1, 0);
+    for (int i = 0; i < n_req; ++i) rec_ptr[i + 1] = rec_ptr[i] + (occ[i] > 1 ? occ[i] : 0);
+    {
+        std::vector<int32_t> next(rec_ptr.begin(), rec_ptr.end() - 1);
+        for (auto& m : members) m.rec = occ[m.row] > 1 ? next[m.row]++ : -1;
+    }
+    const int32_t n_records = rec_ptr[n_req];
+
+    // ---- 5. work items and the static LPT schedule over n_teams
+    const int32_t n_desc = int32_t(descs.size());
+    std::vector<Item> items;
+    items.reserve(size_t(n_desc) * Hkv);
+    for (int32_t d = 0; d < n_desc; ++d)
+        for (int h = 0; h < Hkv; ++h) items.push_back(Item{d, h});
+    const int32_t n_items = int32_t(items.size());
+    std::vector<int32_t> order(n_items);
+    std::iota(order.begin(), order.end(), 0);
+    auto cost = [&](int32_t it) { return int64_t(descs[items[it].desc].n_pages) + 1; };
+    std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return cost(x) > cost(y); });
+    const int T = P->n_teams;
+    std::vector<int32_t> owner(n_items);
+    {
+        using LT = std::pair<int64_t, int32_t>;
+        std::priority_queue<LT, std::vector<LT>, std::greater<LT>> heap;
+        for (int t = 0; t < T; ++t) heap.push({0, t});
+        for (int32_t it : order) {
+            LT top = heap.top();
+            heap.pop();
+            owner[it] = top.second;
+            heap.push({top.first + cost(it), top.second});
+        }
+    }
+    std::vector<int32_t> team_ptr(T + 1, 0), team_items(n_items);
+    for (int32_t it = 0; it < n_items; ++it) team_ptr[owner[it] + 1]++;
+    for (int t = 0; t < T; ++t) team_ptr[t + 1] += team_ptr[t];
+    {
+        std::vector<int32_t> fill(team_ptr.begin(), team_ptr.end() - 1);
+        for (int32_t it : order) team_items[fill[owner[it]]++] = it;   // largest first per team
+    }
+
+    // ---- 6. serialise: header + arrays (int32 words)
+    std::vector<int32_t>& H = P->host;
+    H.assign(H_WORDS, 0);
+    auto put = [&](int slot, const void* src, size_t words) {
+        H[slot] = int32_t(H.size());
+        const int32_t* w = static_cast<const int32_t*>(src);
+        H.insert(H.end(), w, w + words);
+        while (H.size() % 4) H.push_back(0);   // 16-B alignment of every array
+    };
+    put(H_OFF_DESC, descs.data(), descs.size() * 8);
+    put(H_OFF_MEMBER, members.data(), members.size() * 4);
+    put(H_OFF_ITEM, items.data(), items.size() * 2);
+    put(H_OFF_TEAM_PTR, team_ptr.data(), team_ptr.size());
+    put(H_OFF_TEAM_ITEMS, team_items.data(), team_items.size());
+    put(H_OFF_PAGES, pages.data(), pages.size());
+    put(H_OFF_REC_PTR, rec_ptr.data(), rec_ptr.size());
+    H[H_N_REQ] = n_req;
+    H[H_N_DESC] = n_desc;
+    H[H_N_ITEMS] = n_items;
+    H[H_N_TEAMS] = T;
+    H[H_N_RECORDS] = n_records;
+    H[H_N_MEMBERS] = int32_t(members.size());
+    H[H_N_PAGES] = int32_t(pages.size());
+    H[H_TOTAL] = int32_t(H.size());
+
+    int rows_max = 0;
+    for (const auto& d : descs) rows_max = std::max(rows_max, d.n_members * G);
+    spa_plan_stats& st = P->stats;
+    st.n_req = n_req;
+    st.n_groups = n_groups;
+    st.n_desc = n_desc;
+    st.n_items = n_items;
+    st.n_records = n_records;
+    st.n_teams = T;
+    st.rows_max = rows_max;
+    st.unique_tokens = unique_tokens;
+    st.unshared_tokens = unshared_tokens;
+    st.pages_read = pages_read;
+    P->window = window;
+    P->n_req = n_req;
+
+    if (!pool->metadata_only) {
+        int err = plan_upload(P, stream);
+        if (err) return fail(SPA_ERR_CUDA, std::string("plan upload: ") + cuda_error_string(err));
+    }
+    st.generation = P->generation;
+    return SPA_OK;
+}
+
+spa_status spa_plan_get_stats(const spa_plan* plan, spa_plan_stats* out) {
+    if (!plan || !out) return fail(SPA_ERR_INVALID_ARG, "null argument");
+    *out = plan->stats;
+    return SPA_OK;
+}
+
+spa_status spa_plan_debug_array(const spa_plan* plan, int32_t which, const int32_t** out_data, int64_t* out_len,
+                                int32_t* out_row_width) {
+    if (!plan || !out_data || !out_len) return fail(SPA_ERR_INVALID_ARG, "null argument");
+    const auto& H = plan->host;
+    if (H.size() < size_t(H_WORDS)) return fail(SPA_ERR_INVALID_ARG, "plan has not been built");
+    int slot = 0, width = 1;
+    int64_t n = 0;
+    switch (which) {
+        case SPA_DBG_DESC: slot = H_OFF_DESC; width = 8; n = H[H_N_DESC]; break;
+        case SPA_DBG_MEMBER: slot = H_OFF_MEMBER; width = 4; n = H[H_N_MEMBERS]; break;
+        case SPA_DBG_ITEM: slot = H_OFF_ITEM; width = 2; n = H[H_N_ITEMS]; break;
+        case SPA_DBG_TEAM_PTR: slot = H_OFF_TEAM_PTR; n = H[H_N_TEAMS] + 1; break;
+        case SPA_DBG_TEAM_ITEMS: slot = H_OFF_TEAM_ITEMS; n = H[H_N_ITEMS]; break;
+        case SPA_DBG_PAGES: slot = H_OFF_PAGES; n = H[H_N_PAGES]; break;
+        case SPA_DBG_REC_PTR: slot = H_OFF_REC_PTR; n = H[H_N_REQ] + 1; break;
+        default: return fail(SPA_ERR_INVALID_ARG, "unknown debug array");
+    }
+    *out_data = H.data() + H[slot];
+    *out_len = n * width;
+    if (out_row_width) *out_row_width = width;
+    return SPA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,136 @@
+// Internal declarations shared by the host core (pool.cpp, plan.cpp, api.cpp, comm.cpp)
+// and the CUDA kernels (kernels.cu).  Nothing here is part of the public ABI.
+#pragma once
+
+#include <cstdint>
+#include <set>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/spa.h"
+
+namespace spa {
+
+// ---------------------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+spa_status fail(spa_status st, const std::string& msg);
+
+// ---------------------------------------------------------------------------- plan metadata
+// Device plan = one int32 array: a header, then the arrays below at the header offsets.
+enum MetaHeader : int {
+    H_N_REQ = 0,
+    H_N_DESC = 1,
+    H_N_ITEMS = 2,
+    H_N_TEAMS = 3,
+    H_N_RECORDS = 4,
+    H_OFF_DESC = 5,
+    H_OFF_MEMBER = 6,
+    H_OFF_ITEM = 7,
+    H_OFF_TEAM_PTR = 8,
+    H_OFF_TEAM_ITEMS = 9,
+    H_OFF_PAGES = 10,
+    H_OFF_REC_PTR = 11,
+    H_TOTAL = 12,
+    H_N_MEMBERS = 13,
+    H_N_PAGES = 14,
+    H_WORDS = 16
+};
+
+// Work descriptor: keys [tok_start, tok_end) of one group-split or member-tail-split,
+// read through pages[page_off .. page_off + n_pages) (tok_start = first page * ps).
+struct Desc {
+    int32_t page_off, n_pages, tok_start, tok_end, member_off, n_members, kind, group;
+};
+static_assert(sizeof(Desc) == 32, "Desc is 8 int32");
+
+// One request (batch row) taking part in a descriptor.
+struct Member {
+    int32_t row;   // batch row (index into q / o / lse)
+    int32_t lo;    // window lower bound: keys j < lo are masked for this member
+    int32_t rec;   // partial record index, or -1: write final O / LSE directly
+    int32_t pad;
+};
+
+struct Item {
+    int32_t desc, kv_head;
+};
+
+constexpr int kPageSize = 16;          // tokens per page the kernels implement
+constexpr int kPagesPerStage = 2;      // pages of one (KV head) streamed per pipeline stage
+constexpr int kWarps = 4;              // warps per CTA of the decode kernel
+constexpr int kSmemBudget = 196 * 1024;
+
+// ---------------------------------------------------------------------------- pool
+struct Request {
+    std::vector<int32_t> pages;
+    int32_t len = 0;
+};
+
+}  // namespace spa
+
+// CUtensorMap is 128 bytes, 64-B aligned; kept opaque here so host files need no cuda.h.
+struct spa_tmap {
+    alignas(64) unsigned char bytes[128];
+};
+
+struct spa_pool {
+    spa_pool_config cfg;
+    void* k_pool = nullptr;
+    void* v_pool = nullptr;
+    bool metadata_only = true;
+    int device = -1;
+    int sm_count = 0;
+    std::unordered_map<int64_t, spa::Request> reqs;
+    int64_t next_id = 1;
+    std::vector<int32_t> refcount;
+    std::set<int32_t> free_set;
+    spa_tmap tmap_k, tmap_v;
+};
+
+struct spa_plan {
+    spa_pool* pool = nullptr;
+    spa_plan_config cfg{};
+    int mt = 1;                 // m16 tiles (warps) per team: max_rows / 16
+    int n_teams = 0;
+    int num_ctas = 0;
+    // host view of the last plan
+    std::vector<int32_t> host;  // header + arrays (also the upload source, pinned copy below)
+    int32_t* pinned = nullptr;
+    size_t pinned_words = 0;
+    void* upload_event = nullptr;  // cudaEvent_t
+    bool upload_pending = false;
+    // device buffers (grow only)
+    int32_t* d_meta = nullptr;
+    size_t d_meta_words = 0;
+    float* d_part_o = nullptr;
+    float* d_part_lse = nullptr;
+    size_t part_records = 0;
+    int generation = 0;
+    spa_plan_stats stats{};
+    int32_t window = 0;
+    int32_t n_req = 0;
+};
+
+struct spa_comm {
+    void* nccl_comm = nullptr;
+    int rank = 0, world = 1;
+};
+
+namespace spa {
+// kernels.cu launchers (all return cudaError_t as int)
+int launch_append(const spa_pool* pool, const void* k_new, const void* v_new, int32_t T_total,
+                  const std::vector<int32_t>& dst_slots, void* stream);
+int launch_cow(const spa_pool* pool, int32_t src_page, int32_t dst_page, int32_t rows, void* stream);
+int launch_decode(const spa_plan* plan, int32_t layer, const void* q, int64_t q_sr, int64_t q_sh, void* o,
+                  int64_t o_sr, int64_t o_sh, float* lse, int64_t l_sr, int64_t l_sh, float scale, void* stream);
+int launch_merge(int32_t n_req, int32_t num_heads, int32_t head_dim, const int32_t* rec_ptr, const float* part_o,
+                 const float* part_lse, void* o, int64_t o_sr, int64_t o_sh, float* lse, int64_t l_sr, int64_t l_sh,
+                 int grid_hint, void* stream);
+int memset_pool(spa_pool* pool);
+bool make_tensor_maps(spa_pool* pool, std::string* err);
+int device_sm_count(int* device_out);
+const char* cuda_error_string(int err);
+int stages_per_team(int head_dim, int mt);
+size_t decode_smem_bytes(int head_dim, int mt);
+}  // namespace spa

@@ -1,0 +1,357 @@
+"""Thin ctypes binding of libspa.so (include/spa.h).  Argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels; there is no CPU or
+PyTorch fallback: if libspa.so is missing, importing anything that needs it raises.
+PyTorch is used only for device memory, streams and process groups (tensors are passed
+to the library as raw pointers + element strides).
+
+The same names as the C ABI are exported (spa_kv_alloc, spa_kv_append, ...), plus small
+convenience classes (Pool, Plan, Comm) that own the handles.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libspa.so")
+
+SPA_OK, SPA_ERR_INVALID_ARG, SPA_ERR_NO_PAGES, SPA_ERR_BAD_REQUEST = 0, 1, 2, 3
+SPA_ERR_CUDA, SPA_ERR_NCCL, SPA_ERR_UNSUPPORTED, SPA_ERR_NO_DEVICE = 4, 5, 6, 7
+
+c_int32, c_int64, c_void_p, c_float = ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_float
+P_int32 = ctypes.POINTER(c_int32)
+P_int64 = ctypes.POINTER(c_int64)
+
+
+class SpaError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"spa status {status}: {message}")
+        self.status = status
+        self.message = message
+
+
+class spa_pool_config(ctypes.Structure):
+    _fields_ = [("num_layers", c_int32), ("num_q_heads", c_int32), ("num_kv_heads", c_int32),
+                ("head_dim", c_int32), ("page_size", c_int32), ("num_pages", c_int32)]
+
+
+class spa_plan_config(ctypes.Structure):
+    _fields_ = [("sharing", c_int32), ("max_rows", c_int32), ("split_pages", c_int32), ("num_ctas", c_int32)]
+
+
+class spa_plan_stats(ctypes.Structure):
+    _fields_ = [("n_req", c_int32), ("n_groups", c_int32), ("n_desc", c_int32), ("n_items", c_int32),
+                ("n_records", c_int32), ("n_teams", c_int32), ("rows_max", c_int32), ("generation", c_int32),
+                ("unique_tokens", c_int64), ("unshared_tokens", c_int64), ("pages_read", c_int64)]
+
+
+# name -> (restype, argtypes); mirrors include/spa.h and include/spa_debug.h
+_SIGS = {
+    "spa_pool_create": (c_int32, [ctypes.POINTER(spa_pool_config), c_void_p, c_void_p, ctypes.POINTER(c_void_p)]),
+    "spa_pool_destroy": (c_int32, [c_void_p]),
+    "spa_kv_alloc": (c_int32, [c_void_p, P_int64]),
+    "spa_kv_append": (c_int32, [c_void_p, c_int32, P_int64, P_int32, c_void_p, c_void_p, c_void_p]),
+    "spa_fork_request": (c_int32, [c_void_p, c_int64, c_int32, P_int64, c_void_p]),
+    "spa_kv_free": (c_int32, [c_void_p, c_int64]),
+    "spa_kv_page_table": (c_int32, [c_void_p, c_int64, P_int32, c_int32, P_int32, P_int32]),
+    "spa_pool_refcounts": (c_int32, [c_void_p, P_int32]),
+    "spa_pool_free_pages": (c_int32, [c_void_p, P_int32, c_int32, P_int32]),
+    "spa_plan_create": (c_int32, [c_void_p, ctypes.POINTER(spa_plan_config), ctypes.POINTER(c_void_p)]),
+    "spa_plan_destroy": (c_int32, [c_void_p]),
+    "spa_decode_plan": (c_int32, [c_void_p, c_int32, P_int64, c_int32, c_void_p]),
+    "spa_plan_get_stats": (c_int32, [c_void_p, ctypes.POINTER(spa_plan_stats)]),
+    "spa_decode_attention": (c_int32, [c_void_p, c_int32, c_void_p, c_int64, c_int64, c_void_p, c_int64, c_int64,
+                                       c_void_p, c_int64, c_int64, c_float, c_void_p]),
+    "spa_merge_splits": (c_int32, [c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_int64,
+                                   c_int64, c_void_p, c_int64, c_int64, c_void_p]),
+    "spa_nccl_unique_id": (c_int32, [c_void_p]),
+    "spa_comm_create": (c_int32, [c_void_p, c_int32, c_int32, ctypes.POINTER(c_void_p)]),
+    "spa_comm_destroy": (c_int32, [c_void_p]),
+    "spa_decode_attention_sharded": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_int64, c_int64, c_void_p,
+                                               c_void_p, c_float, c_void_p]),
+    "spa_abi_version": (c_int32, []),
+    "spa_last_error": (ctypes.c_char_p, []),
+    "spa_plan_debug_array": (c_int32, [c_void_p, c_int32, ctypes.POINTER(P_int32), P_int64, P_int32]),
+}
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libspa.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run `python -m paper_2511_20048_b200.build` "
+                               "(there is no CPU fallback)")
+        if "SPA_NCCL_LIB" not in os.environ:
+            try:
+                import nvidia.nccl  # noqa: WPS433
+                cand = os.path.join(list(nvidia.nccl.__path__)[0], "lib", "libnccl.so.2")
+                if os.path.exists(cand):
+                    os.environ["SPA_NCCL_LIB"] = cand
+            except ImportError:
+                pass
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != SPA_OK:
+        raise SpaError(status, lib().spa_last_error().decode(errors="replace"))
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch  # noqa: WPS433
+
+        if not torch.cuda.is_available():
+            return None
+        return c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return c_void_p(stream)
+    return c_void_p(stream.cuda_stream)
+
+
+def _ptr(t):
+    return None if t is None else c_void_p(t.data_ptr())
+
+
+# ---------------------------------------------------------------------------- same-name wrappers
+def spa_abi_version() -> int:
+    return lib().spa_abi_version()
+
+
+def spa_pool_create(cfg: spa_pool_config, k_pool_ptr, v_pool_ptr):
+    h = c_void_p()
+    _check(lib().spa_pool_create(ctypes.byref(cfg), k_pool_ptr, v_pool_ptr, ctypes.byref(h)))
+    return h
+
+
+def spa_pool_destroy(h):
+    _check(lib().spa_pool_destroy(h))
+
+
+def spa_kv_alloc(pool_h) -> int:
+    r = c_int64()
+    _check(lib().spa_kv_alloc(pool_h, ctypes.byref(r)))
+    return r.value
+
+
+def spa_kv_append(pool_h, reqs, n_new, k_new_ptr, v_new_ptr, stream_ptr):
+    n = len(reqs)
+    ra = (c_int64 * max(n, 1))(*reqs)
+    na = (c_int32 * max(n, 1))(*n_new)
+    return lib().spa_kv_append(pool_h, n, ra, na, k_new_ptr, v_new_ptr, stream_ptr)
+
+
+def spa_fork_request(pool_h, parent: int, prefix_len: int, stream_ptr):
+    c = c_int64()
+    st = lib().spa_fork_request(pool_h, parent, prefix_len, ctypes.byref(c), stream_ptr)
+    return st, c.value
+
+
+def spa_kv_free(pool_h, req: int):
+    return lib().spa_kv_free(pool_h, req)
+
+
+def spa_kv_page_table(pool_h, req: int):
+    n = c_int32()
+    ln = c_int32()
+    st = lib().spa_kv_page_table(pool_h, req, None, 0, ctypes.byref(n), ctypes.byref(ln))
+    if st != SPA_OK:
+        return st, None, None
+    buf = (c_int32 * max(n.value, 1))()
+    _check(lib().spa_kv_page_table(pool_h, req, buf, n.value, ctypes.byref(n), ctypes.byref(ln)))
+    return st, list(buf[:n.value]), ln.value
+
+
+# ---------------------------------------------------------------------------- classes
+class Pool:
+    """A paged KV pool.  device=None -> metadata-only pool (host logic only)."""
+
+    def __init__(self, num_layers, num_q_heads, num_kv_heads, head_dim, num_pages, page_size=16, device=None):
+        self.cfg = spa_pool_config(num_layers, num_q_heads, num_kv_heads, head_dim, page_size, num_pages)
+        self.k = self.v = None
+        if device is not None:
+            import torch  # noqa: WPS433
+
+            shape = (num_layers, num_pages, num_kv_heads, page_size, head_dim)
+            self.k = torch.empty(shape, dtype=torch.bfloat16, device=device)
+            self.v = torch.empty(shape, dtype=torch.bfloat16, device=device)
+        self.h = spa_pool_create(self.cfg, _ptr(self.k), _ptr(self.v))
+
+    @property
+    def num_pages(self):
+        return self.cfg.num_pages
+
+    def close(self):
+        if self.h:
+            spa_pool_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 (interpreter shutdown)
+            pass
+
+    def alloc(self) -> int:
+        return spa_kv_alloc(self.h)
+
+    def append(self, reqs, n_new, k_new=None, v_new=None, stream=None, check=True):
+        """k_new, v_new: bf16 tensors [L, sum(n_new), Hkv, d] (contiguous)."""
+        for t in (k_new, v_new):
+            if t is not None and not t.is_contiguous():
+                raise ValueError("k_new / v_new must be contiguous")
+        st = spa_kv_append(self.h, list(reqs), list(n_new), _ptr(k_new), _ptr(v_new),
+                           _stream_ptr(stream) if self.k is not None else None)
+        if check:
+            _check(st)
+        return st
+
+    def fork(self, parent, prefix_len, stream=None, check=True):
+        st, child = spa_fork_request(self.h, parent, prefix_len, _stream_ptr(stream) if self.k is not None else None)
+        if check:
+            _check(st)
+            return child
+        return st, child
+
+    def free(self, req, check=True):
+        st = spa_kv_free(self.h, req)
+        if check:
+            _check(st)
+        return st
+
+    def page_table(self, req):
+        return spa_kv_page_table(self.h, req)
+
+    def refcounts(self):
+        buf = (c_int32 * self.cfg.num_pages)()
+        _check(lib().spa_pool_refcounts(self.h, buf))
+        return list(buf)
+
+    def free_pages(self):
+        n = c_int32()
+        buf = (c_int32 * self.cfg.num_pages)()
+        _check(lib().spa_pool_free_pages(self.h, buf, self.cfg.num_pages, ctypes.byref(n)))
+        return list(buf[:n.value])
+
+
+class Plan:
+    def __init__(self, pool: Pool, sharing=True, max_rows=16, split_pages=0, num_ctas=0):
+        self.pool = pool
+        cfg = spa_plan_config(1 if sharing else 0, max_rows, split_pages, num_ctas)
+        h = c_void_p()
+        _check(lib().spa_plan_create(pool.h, ctypes.byref(cfg), ctypes.byref(h)))
+        self.h = h
+        self.n_req = 0
+
+    def close(self):
+        if self.h:
+            _check(lib().spa_plan_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    def plan(self, reqs, window=0, stream=None, check=True):
+        n = len(reqs)
+        ra = (c_int64 * max(n, 1))(*reqs)
+        st = lib().spa_decode_plan(self.h, n, ra, int(window),
+                                   _stream_ptr(stream) if self.pool.k is not None else None)
+        if check:
+            _check(st)
+            self.n_req = n
+        return st
+
+    def stats(self) -> dict:
+        s = spa_plan_stats()
+        _check(lib().spa_plan_get_stats(self.h, ctypes.byref(s)))
+        return {f: getattr(s, f) for f, _ in s._fields_}
+
+    def debug_array(self, which: int):
+        data = P_int32()
+        n = c_int64()
+        w = c_int32()
+        _check(lib().spa_plan_debug_array(self.h, which, ctypes.byref(data), ctypes.byref(n), ctypes.byref(w)))
+        flat = [data[i] for i in range(n.value)]
+        if w.value > 1:
+            return [flat[i:i + w.value] for i in range(0, len(flat), w.value)]
+        return flat
+
+    def decode(self, layer, q, o=None, lse=None, scale=None, stream=None, want_lse=True):
+        """q: bf16 [N, Hq, d] (any strides, d contiguous).  Returns (o, lse)."""
+        import torch  # noqa: WPS433
+
+        N, Hq, d = q.shape
+        if scale is None:
+            scale = d ** -0.5
+        if o is None:
+            o = torch.empty((N, Hq, d), dtype=torch.bfloat16, device=q.device)
+        if lse is None and want_lse:
+            lse = torch.empty((N, Hq), dtype=torch.float32, device=q.device)
+        if q.stride(2) != 1 or o.stride(2) != 1:
+            raise ValueError("head_dim must be contiguous")
+        _check(lib().spa_decode_attention(
+            self.h, int(layer), _ptr(q), q.stride(0), q.stride(1), _ptr(o), o.stride(0), o.stride(1),
+            _ptr(lse), lse.stride(0) if lse is not None else 0, lse.stride(1) if lse is not None else 0,
+            float(scale), _stream_ptr(stream)))
+        return o, lse
+
+    def decode_sharded(self, comm, layer, q_local, o_gathered, lse_gathered=None, scale=None, stream=None):
+        d = q_local.shape[-1]
+        if scale is None:
+            scale = d ** -0.5
+        _check(lib().spa_decode_attention_sharded(
+            self.h, comm.h, int(layer), _ptr(q_local), q_local.stride(0), q_local.stride(1),
+            _ptr(o_gathered), _ptr(lse_gathered), float(scale), _stream_ptr(stream)))
+        return o_gathered, lse_gathered
+
+
+def spa_merge_splits(rec_ptr, part_o, part_lse, o, lse=None, stream=None):
+    """rec_ptr int32 [N+1], part_o fp32 [S, H, d], part_lse fp32 [S, H] (device tensors)."""
+    N = rec_ptr.numel() - 1
+    S, H, d = part_o.shape
+    _check(lib().spa_merge_splits(N, H, d, _ptr(rec_ptr), _ptr(part_o), _ptr(part_lse), _ptr(o), o.stride(0),
+                                  o.stride(1), _ptr(lse), lse.stride(0) if lse is not None else 0,
+                                  lse.stride(1) if lse is not None else 0, _stream_ptr(stream)))
+    return o, lse
+
+
+def shard_heads(num_q_heads: int, num_kv_heads: int, rank: int, world: int):
+    """KV-head sharding: rank r holds KV heads [r Hkv/n, (r+1) Hkv/n)
+    and the query heads that read them, [r Hq/n, (r+1) Hq/n) (kv = floor(h / G), reading #5)."""
+    if num_kv_heads % world or num_q_heads % num_kv_heads:
+        raise ValueError("world must divide num_kv_heads and num_kv_heads must divide num_q_heads")
+    hkv, hq = num_kv_heads // world, num_q_heads // world
+    return slice(rank * hq, (rank + 1) * hq), slice(rank * hkv, (rank + 1) * hkv)
+
+
+def spa_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().spa_nccl_unique_id(buf))
+    return buf.raw
+
+
+class Comm:
+    def __init__(self, unique_id: bytes, rank: int, world: int):
+        h = c_void_p()
+        buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+        _check(lib().spa_comm_create(buf, rank, world, ctypes.byref(h)))
+        self.h = h
+        self.rank, self.world = rank, world
+
+    def close(self):
+        if self.h:
+            _check(lib().spa_comm_destroy(self.h))
+            self.h = None

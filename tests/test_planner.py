@@ -1,0 +1,173 @@
+"""Host planner invariants (metadata-only pools, CPU only).
+
+For every batch row r and KV head h the work descriptors containing r must cover its
+attended keys [lo_r, n_r) exactly once (with the member's lower bound applied), read
+each key through the right physical page, and the static schedule must run every item
+exactly once.  With sharing on, a shared page is read once per (KV head, group).
+"""
+import numpy as np
+import pytest
+from hypothesis import given, settings
+from hypothesis import strategies as st
+
+from paper_2511_20048_b200 import spa
+from paper_2511_20048_b200.spa import SpaError
+from spa_inputs import workloads
+
+DBG_DESC, DBG_MEMBER, DBG_ITEM, DBG_TEAM_PTR, DBG_TEAM_ITEMS, DBG_PAGES, DBG_REC_PTR = range(7)
+
+
+def build(recipe, num_pages=None):
+    m = recipe.model
+    ops, batch = workloads.call_log(recipe)
+    need = sum(-(-(g.prefix + max([g.parent_tail or 0] + g.fork_tails)) // 16) * (1 + len(g.fork_tails))
+               for g in recipe.groups) + 16
+    pool = spa.Pool(1, m.num_q_heads, m.num_kv_heads, m.head_dim, num_pages or need)
+    ids = {}
+    for op in ops:
+        if op[0] == "alloc":
+            ids[op[1]] = pool.alloc()
+        elif op[0] == "append":
+            pool.append([ids[op[1]]], [op[4]])
+        elif op[0] == "fork":
+            ids[op[1]] = pool.fork(ids[op[2]], op[3])
+    return pool, [ids[n] for n in batch]
+
+
+def check_plan(pool, plan, reqs, window):
+    descs = plan.debug_array(DBG_DESC)
+    mems = plan.debug_array(DBG_MEMBER)
+    items = plan.debug_array(DBG_ITEM)
+    tptr = plan.debug_array(DBG_TEAM_PTR)
+    titems = plan.debug_array(DBG_TEAM_ITEMS)
+    pages = plan.debug_array(DBG_PAGES)
+    rec_ptr = plan.debug_array(DBG_REC_PTR)
+    Hkv = pool.cfg.num_kv_heads
+    N = len(reqs)
+    tables = [pool.page_table(r) for r in reqs]
+    cover = [dict() for _ in range(N)]   # token -> count
+    occ = [0] * N
+    recs = [[] for _ in range(N)]
+    for d in descs:
+        page_off, n_pages, t0, t1, moff, nmem, kind, group = d
+        assert t0 % 16 == 0 and t1 <= t0 + 16 * n_pages and t1 > t0 + 16 * (n_pages - 1)
+        for mi in range(moff, moff + nmem):
+            row, lo, rec, _ = mems[mi]
+            occ[row] += 1
+            recs[row].append(rec)
+            _, tab, n = tables[row]
+            assert lo == (max(0, n - window) if window > 0 else 0)
+            for t in range(max(t0, lo), t1):
+                assert pages[page_off + (t - t0) // 16] == tab[t // 16], "wrong physical page"
+                cover[row][t] = cover[row][t] + 1 if t in cover[row] else 1
+    for r in range(N):
+        _, tab, n = tables[r]
+        lo = max(0, n - window) if window > 0 else 0
+        assert sorted(cover[r]) == list(range(lo, n)), r
+        assert all(c == 1 for c in cover[r].values())
+        if occ[r] == 1:
+            assert recs[r] == [-1] and rec_ptr[r + 1] == rec_ptr[r]
+        else:
+            assert sorted(recs[r]) == list(range(rec_ptr[r], rec_ptr[r + 1]))
+    assert len(items) == len(descs) * Hkv
+    assert sorted((a, b) for a, b in items) == sorted((d, h) for d in range(len(descs)) for h in range(Hkv))
+    assert sorted(titems) == list(range(len(items)))
+    assert tptr[0] == 0 and tptr[-1] == len(items) and all(a <= b for a, b in zip(tptr, tptr[1:]))
+    return descs, mems
+
+
+@settings(max_examples=80, deadline=None)
+@given(st.integers(0, 100_000), st.sampled_from([0, 0, 1, 7, 16, 40, 300]), st.booleans(),
+       st.sampled_from([16, 32]), st.sampled_from([0, 1, 3]))
+def test_random_batches_cover_every_key_once(seed, window, sharing, max_rows, split):
+    rec = workloads.random_small(seed)
+    pool, reqs = build(rec)
+    G = rec.model.num_q_heads // rec.model.num_kv_heads
+    if G > max_rows:
+        return
+    plan = spa.Plan(pool, sharing=sharing, max_rows=max_rows, split_pages=split, num_ctas=3)
+    plan.plan(reqs, window)
+    check_plan(pool, plan, reqs, window)
+
+
+def test_shared_prefix_read_once_per_group_and_head():
+    rec = workloads.qwen(seed=1)
+    pool, reqs = build(rec)
+    plan = spa.Plan(pool, num_ctas=148)
+    plan.plan(reqs)
+    descs, mems = check_plan(pool, plan, reqs, 0)
+    s = plan.stats()
+    # every group: one parent + one fork with a >= 2048-token shared prefix
+    assert s["n_groups"] == 32 and s["rows_max"] == 10
+    shared_tokens = sum(g.prefix // 16 * 16 for g in rec.groups)
+    tail_tokens = sum(g.prefix % 16 * 2 + g.parent_tail + g.fork_tails[0] for g in rec.groups)
+    assert s["unique_tokens"] == shared_tokens + tail_tokens
+    assert s["unshared_tokens"] == sum(2 * g.prefix + g.parent_tail + g.fork_tails[0] for g in rec.groups)
+    assert s["unshared_tokens"] / s["unique_tokens"] > 1.9
+
+
+def test_sharing_off_is_groups_of_one():
+    rec = workloads.qwen(seed=1, n_agents=4)
+    pool, reqs = build(rec)
+    plan = spa.Plan(pool, sharing=False, num_ctas=8)
+    plan.plan(reqs)
+    descs, _ = check_plan(pool, plan, reqs, 0)
+    assert all(d[5] == 1 for d in descs)
+    s = plan.stats()
+    assert s["unique_tokens"] == s["unshared_tokens"]
+
+
+def test_subgroups_when_rows_exceed_max_rows():
+    rec = workloads.sweep(16, 0.75)         # parents with 3 forks: 4 x 5 = 20 rows
+    pool, reqs = build(rec)
+    p16 = spa.Plan(pool, max_rows=16, num_ctas=4)
+    p16.plan(reqs)
+    p32 = spa.Plan(pool, max_rows=32, num_ctas=4)
+    p32.plan(reqs)
+    check_plan(pool, p16, reqs, 0)
+    check_plan(pool, p32, reqs, 0)
+    assert p16.stats()["rows_max"] <= 16 and p32.stats()["rows_max"] == 20
+    assert p32.stats()["unique_tokens"] < p16.stats()["unique_tokens"]
+
+
+def test_window_restricts_to_union_of_windows():
+    rec = workloads.gemma(seed=2, n_agents=6)
+    pool, reqs = build(rec)
+    plan = spa.Plan(pool, num_ctas=16)
+    plan.plan(reqs, window=1024)
+    check_plan(pool, plan, reqs, 1024)
+    s = plan.stats()
+    assert s["unshared_tokens"] == 1024 * len(reqs)
+
+
+def test_plan_errors():
+    pool = spa.Pool(1, 4, 2, 64, 8)
+    a = pool.alloc()
+    b = pool.alloc()
+    pool.append([a], [5])
+    plan = spa.Plan(pool)
+    with pytest.raises(SpaError) as e:
+        plan.plan([a, a])
+    assert e.value.status == spa.SPA_ERR_INVALID_ARG
+    with pytest.raises(SpaError) as e:
+        plan.plan([a, b])                 # b is empty
+    assert e.value.status == spa.SPA_ERR_INVALID_ARG
+    with pytest.raises(SpaError) as e:
+        plan.plan([a, 999])
+    assert e.value.status == spa.SPA_ERR_BAD_REQUEST
+    with pytest.raises(SpaError) as e:
+        spa.Plan(pool, max_rows=24)
+    assert e.value.status == spa.SPA_ERR_UNSUPPORTED
+
+
+def test_lpt_schedule_is_balanced():
+    rec = workloads.qwen(seed=1)
+    pool, reqs = build(rec)
+    plan = spa.Plan(pool, num_ctas=148)
+    plan.plan(reqs)
+    descs = plan.debug_array(DBG_DESC)
+    items = plan.debug_array(DBG_ITEM)
+    tptr = plan.debug_array(DBG_TEAM_PTR)
+    titems = plan.debug_array(DBG_TEAM_ITEMS)
+    loads = [sum(descs[items[i][0]][1] + 1 for i in titems[a:b]) for a, b in zip(tptr, tptr[1:])]
+    assert max(loads) <= 1.15 * np.mean(loads)
