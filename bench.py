@@ -45,7 +45,13 @@ def parse():
     ap.add_argument("--impl", default="spa", choices=["spa", "reference"])
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="cudaProfilerStart/Stop around the timed steps only (ncu --profile-from-start off); "
+                         "skips parity, e2e and the cpu baseline")
     ap.add_argument("--sharing", type=int, default=1)
+    ap.add_argument("--fused-merge", action="store_true",
+                    help="merge split partials inside the decode kernel (default: PDL-chained merge kernel)")
+    ap.add_argument("--split-pages", type=int, default=0, help="max pages per split (0 = auto)")
     ap.add_argument("--layers", type=int, default=0, help="override resident layer count (0 = model's)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the oracle cpu_baseline sample")
     return ap.parse_args()
@@ -264,7 +270,8 @@ def run_spa(args):
         comm = None
         o_all = torch.empty((L, N, hq_l, d), dtype=torch.bfloat16, device=dev)
         lse_all = torch.empty((L, N, hq_l), dtype=torch.float32, device=dev)
-    plan = spa.Plan(pool, sharing=bool(args.sharing))
+    plan = spa.Plan(pool, sharing=bool(args.sharing), split_pages=args.split_pages,
+                    fused_merge=args.fused_merge)
 
     state = {"step": 0}
 
@@ -293,6 +300,8 @@ def run_spa(args):
     parity = None
     one_step(step_k, step_v)
     torch.cuda.synchronize()
+    if args.profile:
+        args.no_parity = args.no_e2e = True
     if not args.no_parity and rank == 0:
         gsel = [0, len(recipe.groups) // 2]
         rows = [i for i, nm in enumerate(batch) if nm[0] in gsel]
@@ -326,11 +335,15 @@ def run_spa(args):
     with clocks:
         time.sleep(0.3)
         barrier()
+        if args.profile:
+            torch.cuda.profiler.start()
         ev0.record(stream)
         for _ in range(args.steps):
             one_step(step_k, step_v)
         ev1.record(stream)
         barrier()
+        if args.profile:
+            torch.cuda.profiler.stop()
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
         t = torch.tensor([ms], device=dev)
@@ -401,9 +414,10 @@ def run_spa(args):
 
     result = None
     if rank == 0:
-        cpu = cpu_baseline(recipe, batch, args.cpu_seconds) if world == 1 else None
+        cpu = cpu_baseline(recipe, batch, args.cpu_seconds) if world == 1 and not args.profile else None
         ck = clocks.summary(local)
-        launches_per_step = (-(-N // 896)) + L * (1 + (1 if st["n_records"] > 0 else 0))
+        sep = (not args.fused_merge) and st["n_records"] > 0
+        launches_per_step = (-(-N // 896)) + L * (2 if sep else 1)
         result = {
             "metric": METRIC,
             "value": N / (ms * 1e-3),
@@ -428,7 +442,8 @@ def run_spa(args):
             "hbm_gbs_algorithmic": achieved,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"], "traffic": None,
-                         "kernel": "spa_decode_attention (decode_kernel + merge_kernel)",
+                         "kernel": ("decode_kernel + merge_kernel (one spa_decode_attention call)" if sep
+                                    else "decode_kernel (split merge fused in-kernel)"),
                          "peak_kind": pk_kind, "alg_bytes_per_launch": int(alg_bytes),
                          "frac_of_8tbs": achieved / 8000.0},
             "sharing": {"unique_tokens_per_kv_head": st["unique_tokens"],

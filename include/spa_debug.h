@@ -10,8 +10,8 @@
  *   SPA_DBG_MEMBER    rows of 4: batch row, window lower bound lo, record (-1 = direct
  *                     output), reserved
  *   SPA_DBG_ITEM      rows of 2: descriptor, local KV head
- *   SPA_DBG_TEAM_PTR  n_teams + 1 offsets into SPA_DBG_TEAM_ITEMS
- *   SPA_DBG_TEAM_ITEMS item indices, team by team (static LPT schedule)
+ *   SPA_DBG_QUEUE     item indices in the order the persistent kernel's teams pop them
+ *                     (dynamic longest-processing-time: largest first)
  *   SPA_DBG_PAGES     page ids referenced by descriptors
  *   SPA_DBG_REC_PTR   n_req + 1 offsets: partial records of batch row i
  */
@@ -28,8 +28,7 @@ enum {
     SPA_DBG_DESC = 0,
     SPA_DBG_MEMBER = 1,
     SPA_DBG_ITEM = 2,
-    SPA_DBG_TEAM_PTR = 3,
-    SPA_DBG_TEAM_ITEMS = 4,
+    SPA_DBG_QUEUE = 3,
     SPA_DBG_PAGES = 5,
     SPA_DBG_REC_PTR = 6
 };

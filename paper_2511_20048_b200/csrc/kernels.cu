@@ -15,6 +15,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "spa_internal.h"
@@ -148,6 +149,12 @@ __device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+__device__ __forceinline__ int atom_add_acq_rel_gpu(int* addr, int v) {
+    int old;
+    asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], %2;" : "=r"(old) : "l"(addr), "r"(v) : "memory");
+    return old;
+}
+
 __device__ __forceinline__ float fast_exp2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -157,6 +164,125 @@ __device__ __forceinline__ float fast_exp2(float x) {
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// Launch with programmatic stream serialization (PDL): the kernel may start while the
+// previous kernel on the stream drains; every kernel here begins with griddepcontrol.wait
+// before touching memory the previous one wrote.  SPA_NO_PDL=1 disables it (A/B runs).
+template <typename... KArgs, typename... Args>
+static int launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, void* stream, Args&&... args) {
+    static const bool no_pdl = std::getenv("SPA_NO_PDL") != nullptr;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = no_pdl ? 0 : 1;
+    return int(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
+// ============================================================================ a6 core: one warp merges one head
+// Split-KV partial-LSE merge of records [s0, s1) of one (request, head) (oracle:
+// merge_partials; include/spa.h spa_merge_splits):
+//     LSE = m + ln sum_{s live} exp(LSE_s - m),  O = sum_s exp(LSE_s - LSE) O_s,
+//     all partials -inf -> O = 0, LSE = -inf.
+// Lanes own records for the LSE reduction (shuffle max / sum) and float4 columns for O;
+// partials are read with ld.global.cg (L2): they were written by other SMs.
+template <int DT>   // DT = head_dim if known at compile time, 0 = runtime `dim`
+__device__ __forceinline__ void warp_merge_head(const float* part_o, const float* part_lse, int H, int s0, int s1,
+                                                int head, __nv_bfloat16* orow, long long o_sh, float* lrow,
+                                                long long l_sh, int lane, int dim = DT) {
+    const int D = DT ? DT : dim;
+    orow += (long long)head * o_sh;
+    if (s1 - s0 <= 32) {
+        // common case: one record per lane, the LSEs are read once (one L2 round trip for
+        // the LSEs, one for the partial O rows, issued back to back)
+        const int S = s1 - s0;
+        const float ls = lane < S ? __ldcg(part_lse + (long long)(s0 + lane) * H + head) : -INFINITY;
+        float m = ls;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        float e = (ls != -INFINITY) ? expf(ls - m) : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+        const float lse = (m == -INFINITY) ? -INFINITY : m + logf(e);
+        const float w = (ls != -INFINITY) ? expf(ls - lse) : 0.f;
+        for (int c = lane * 4; c - lane * 4 < D; c += 128) {
+            float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
+            for (int j = 0; j < S; ++j) {
+                const float wj = __shfl_sync(0xffffffffu, w, j);
+                if (c < D && wj != 0.f) {
+                    const float4 v =
+                        __ldcg(reinterpret_cast<const float4*>(part_o + ((long long)(s0 + j) * H + head) * D + c));
+                    a.x += wj * v.x;
+                    a.y += wj * v.y;
+                    a.z += wj * v.z;
+                    a.w += wj * v.w;
+                }
+            }
+            if (c < D) {
+                *reinterpret_cast<__nv_bfloat162*>(orow + c) = __floats2bfloat162_rn(a.x, a.y);
+                *reinterpret_cast<__nv_bfloat162*>(orow + c + 2) = __floats2bfloat162_rn(a.z, a.w);
+            }
+        }
+        if (lane == 0 && lrow) lrow[(long long)head * l_sh] = lse;
+        return;
+    }
+    float m = -INFINITY;
+    for (int sb = s0; sb < s1; sb += 32) {
+        const int s = sb + lane;
+        if (s < s1) m = fmaxf(m, __ldcg(part_lse + (long long)s * H + head));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    float sum = 0.f;
+    if (m != -INFINITY) {
+        for (int sb = s0; sb < s1; sb += 32) {
+            const int s = sb + lane;
+            if (s < s1) {
+                const float ls = __ldcg(part_lse + (long long)s * H + head);
+                if (ls != -INFINITY) sum += expf(ls - m);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const float lse = (m == -INFINITY) ? -INFINITY : m + logf(sum);
+    for (int c = lane * 4; c - lane * 4 < D; c += 128) {
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (m != -INFINITY) {
+            for (int sb = s0; sb < s1; sb += 32) {
+                const int s = sb + lane;
+                float w = 0.f;
+                if (s < s1) {
+                    const float ls = __ldcg(part_lse + (long long)s * H + head);
+                    if (ls != -INFINITY) w = expf(ls - lse);
+                }
+                const int n = min(32, s1 - sb);
+#pragma unroll 8
+                for (int j = 0; j < n; ++j) {
+                    const float wj = __shfl_sync(0xffffffffu, w, j);
+                    if (c < D) {
+                        const float4 v = __ldcg(reinterpret_cast<const float4*>(part_o + ((long long)(sb + j) * H + head) * D + c));
+                        a.x += wj * v.x;
+                        a.y += wj * v.y;
+                        a.z += wj * v.z;
+                        a.w += wj * v.w;
+                    }
+                }
+            }
+        }
+        if (c < D) {
+            *reinterpret_cast<__nv_bfloat162*>(orow + c) = __floats2bfloat162_rn(a.x, a.y);
+            *reinterpret_cast<__nv_bfloat162*>(orow + c + 2) = __floats2bfloat162_rn(a.z, a.w);
+        }
+    }
+    if (lane == 0 && lrow) lrow[(long long)head * l_sh] = lse;
 }
 
 // ============================================================================ a2: append
@@ -245,6 +371,7 @@ struct DecodeParams {
     float scale_log2;
     int layer_row_base;  // layer * num_pages * Hkv * 16
     int num_q_heads, group_size, num_kv_heads;
+    int fused_merge;     // 1: the last item of a (request, KV head) merges its partials in-kernel
 };
 
 template <int D, int MT>
@@ -254,7 +381,8 @@ struct DecodeCfg {
     static constexpr int STAGE_BYTES = kPagesPerStage * 2 * PAGE_BYTES;
     static constexpr int NS = (kSmemBudget - 1024) / (TEAMS * STAGE_BYTES);
     static constexpr int RING_BYTES = TEAMS * NS * STAGE_BYTES;
-    static constexpr int SMEM = 1024 + RING_BYTES + TEAMS * NS * 2 * 8;
+    static constexpr int QN = NS + 2;   // popped-item queue entries per team
+    static constexpr int SMEM = 1024 + RING_BYTES + TEAMS * NS * 2 * 8 + TEAMS * 4 + TEAMS * QN * 4;
     static_assert(NS >= 2, "pipeline needs >= 2 stages");
 };
 
@@ -285,6 +413,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     const uint32_t bars = smem_u32(smem) + C::RING_BYTES;
     auto full_bar = [&](int s) { return bars + (team * C::NS + s) * 8; };
     auto empty_bar = [&](int s) { return bars + (C::TEAMS * C::NS + team * C::NS + s) * 8; };
+    uint32_t* team_slot = reinterpret_cast<uint32_t*>(smem + C::RING_BYTES + C::TEAMS * C::NS * 2 * 8) + team;
+    int32_t* team_q = reinterpret_cast<int32_t*>(smem + C::RING_BYTES + C::TEAMS * C::NS * 2 * 8 + C::TEAMS * 4);
+    auto team_sync = [&]() {
+        if constexpr (MT == 1) __syncwarp();
+        else asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(MT * 32) : "memory");
+    };
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < C::TEAMS * C::NS; ++i) {
@@ -294,56 +428,82 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    // programmatic dependent launch: everything above overlapped the previous kernel's
+    // tail; from here on we read what it (and earlier stream work) wrote.  Let the next
+    // kernel (the split merge / the next layer) start its own prologue early.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
 
     const int32_t* meta = p.meta;
-    const int gteam = blockIdx.x * C::TEAMS + team;
-    if (gteam >= meta[H_N_TEAMS]) return;
     const Desc* descs = reinterpret_cast<const Desc*>(meta + meta[H_OFF_DESC]);
     const Member* mems = reinterpret_cast<const Member*>(meta + meta[H_OFF_MEMBER]);
     const Item* items = reinterpret_cast<const Item*>(meta + meta[H_OFF_ITEM]);
-    const int32_t* team_items = meta + meta[H_OFF_TEAM_ITEMS];
+    const int32_t* queue = meta + meta[H_OFF_QUEUE];
     const int32_t* pages = meta + meta[H_OFF_PAGES];
-    const int ib = meta[meta[H_OFF_TEAM_PTR] + gteam], ie = meta[meta[H_OFF_TEAM_PTR] + gteam + 1];
-    if (ib >= ie) return;
+    const int32_t* rec_ptr = meta + meta[H_OFF_REC_PTR];
+    int32_t* counters = const_cast<int32_t*>(meta) + meta[H_OFF_COUNTERS];
+    int32_t* sched = const_cast<int32_t*>(meta) + meta[H_OFF_SCHED];
+    const int n_items = meta[H_N_ITEMS];
+    int32_t* tq = team_q + team * C::QN;   // items this team popped, in order (producer -> consumers)
 
     const int G = p.group_size, Hq = p.num_q_heads, Hkv = p.num_kv_heads;
     const bool leader = (wt == 0) && (lane == 0);
     uint64_t policy = 0;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
 
-    // ---- producer (one elected thread per team): stream (item, stage) in order
-    int p_it = ib, p_st = 0;
+    // ---- producer (one elected thread per team): pops items from the dynamic LPT queue
+    //      and streams their (stage) page pairs into the ring, NS stages ahead.  When the
+    //      queue is empty it publishes -1 and completes the slot's barrier without data.
+    int p_item = -1, p_st = 0, p_n = 0;
+    bool p_done = false;
+    Item p_itm{0, 0};
+    Desc p_dsc{};
     auto issue_next = [&](int slot) {
-        if (p_it >= ie) return;
-        const Item itm = items[team_items[p_it]];
-        const Desc dsc = descs[itm.desc];
+        if (p_done) return;
+        if (p_item < 0) {
+            const int qi = atomicAdd(sched, 1);
+            const int it = qi < n_items ? queue[qi] : -1;
+            tq[p_n % C::QN] = it;
+            ++p_n;
+            if (it < 0) {
+                p_done = true;
+                mbar_arrive(full_bar(slot));
+                return;
+            }
+            p_item = it;
+            p_st = 0;
+            p_itm = items[it];
+            p_dsc = descs[p_itm.desc];
+        }
         const int p0 = p_st * PPS;
-        const int npg = min(PPS, dsc.n_pages - p0);
+        const int npg = min(PPS, p_dsc.n_pages - p0);
         const uint32_t fb = full_bar(slot);
         mbar_expect_tx(fb, npg * 2 * C::PAGE_BYTES);
         const uint32_t sb = ring + slot * C::STAGE_BYTES;
         for (int j = 0; j < npg; ++j) {
-            const int page = pages[dsc.page_off + p0 + j];
-            const int row = p.layer_row_base + (page * Hkv + itm.kv_head) * kPageSize;
+            const int page = pages[p_dsc.page_off + p0 + j];
+            const int row = p.layer_row_base + (page * Hkv + p_itm.kv_head) * kPageSize;
 #pragma unroll
             for (int hf = 0; hf < D / 64; ++hf) {
                 tma_load_2d(sb + j * 2 * C::PAGE_BYTES + hf * 2048, &tmk, hf * 64, row, fb, policy);
                 tma_load_2d(sb + j * 2 * C::PAGE_BYTES + C::PAGE_BYTES + hf * 2048, &tmv, hf * 64, row, fb, policy);
             }
         }
-        if (++p_st * PPS >= dsc.n_pages) {
-            p_st = 0;
-            ++p_it;
-        }
+        if (++p_st * PPS >= p_dsc.n_pages) p_item = -1;
     };
     if (leader) {
         for (int s = 0; s < C::NS; ++s) issue_next(s);
     }
 
-    int slot = 0;
+    int slot = 0, c_n = 0;
     uint32_t phase = 0;
-    for (int it = ib; it < ie; ++it) {
-        const Item itm = items[team_items[it]];
+    while (true) {
+        // the first stage of the next item (or the end-of-queue marker) has landed
+        mbar_wait(full_bar(slot), phase);
+        const int it = tq[c_n % C::QN];
+        ++c_n;
+        if (it < 0) break;
+        const Item itm = items[it];
         const Desc dsc = descs[itm.desc];
         const int R = dsc.n_members * G;
         const bool active = wt * 16 < R;
@@ -389,7 +549,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 
         const int nst = (dsc.n_pages + PPS - 1) / PPS;
         for (int st = 0; st < nst; ++st) {
-            mbar_wait(full_bar(slot), phase);
+            if (st > 0) mbar_wait(full_bar(slot), phase);
             if (active) {
                 const uint32_t sb = ring + slot * C::STAGE_BYTES;
                 const int npg = min(PPS, dsc.n_pages - st * PPS);
@@ -538,6 +698,52 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
                 }
             }
         }
+
+        // ---- fused split merge (a6): the last item to finish a (request, KV head) merges
+        //      that request's partial records for the G query heads of this KV head.
+        bool any_partial = false;
+        for (int mb = 0; mb < dsc.n_members; ++mb) any_partial |= mems[dsc.member_off + mb].rec >= 0;
+        if (any_partial && p.fused_merge) {
+            // the team barrier orders every lane's partial stores before the leader's
+            // acq_rel arrival (release is cumulative); the last arriver acquires all of them
+            team_sync();
+            uint32_t mask = 0;
+            if (leader) {
+                for (int mb = 0; mb < dsc.n_members; ++mb) {
+                    const Member mm = mems[dsc.member_off + mb];
+                    if (mm.rec < 0) continue;
+                    const int nrec = rec_ptr[mm.row + 1] - rec_ptr[mm.row];
+                    int* c = counters + mm.row * Hkv + itm.kv_head;
+                    if (atom_add_acq_rel_gpu(c, 1) == nrec - 1) {
+                        mask |= 1u << mb;
+                        *c = 0;    // every arrival of this launch is in: ready for the next layer
+                    }
+                }
+            }
+            if constexpr (MT == 1) {
+                mask = __shfl_sync(0xffffffffu, mask, 0);
+            } else {
+                if (leader) *team_slot = mask;
+                team_sync();
+                mask = *team_slot;
+            }
+            while (mask) {
+                const int mb = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const Member mm = mems[dsc.member_off + mb];
+                for (int hh = wt; hh < G; hh += MT)
+                    warp_merge_head<D>(p.part_o, p.part_lse, Hq, rec_ptr[mm.row], rec_ptr[mm.row + 1],
+                                       itm.kv_head * G + hh, p.o + mm.row * p.o_sr, p.o_sh,
+                                       p.lse ? p.lse + mm.row * p.l_sr : nullptr, p.l_sh, lane);
+            }
+        }
+    }
+    // the last team to drain the queue rewinds it for the next launch (stream-ordered)
+    if (leader) {
+        if (atomicAdd(sched + 1, 1) == int(gridDim.x) * C::TEAMS - 1) {
+            sched[0] = 0;
+            sched[1] = 0;
+        }
     }
 }
 
@@ -555,6 +761,8 @@ struct MergeParams {
 
 // One warp per (request, head); lanes stride over float4 columns.
 __global__ void __launch_bounds__(256) merge_kernel(const MergeParams p) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // partials come from the decode kernel
+    asm volatile("griddepcontrol.launch_dependents;");
     const int warps = (gridDim.x * blockDim.x) >> 5;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -562,36 +770,8 @@ __global__ void __launch_bounds__(256) merge_kernel(const MergeParams p) {
         const int r = pair / p.H, h = pair - r * p.H;
         const int s0 = p.rec_ptr[r], s1 = p.rec_ptr[r + 1];
         if (s0 == s1) continue;
-        float m = -INFINITY;
-        for (int s = s0; s < s1; ++s) m = fmaxf(m, p.part_lse[(long long)s * p.H + h]);
-        __nv_bfloat16* orow = p.o + r * p.o_sr + h * p.o_sh;
-        if (m == -INFINITY) {
-            for (int c = lane * 4; c < p.D; c += 128) {
-                *reinterpret_cast<__nv_bfloat162*>(orow + c) = __floats2bfloat162_rn(0.f, 0.f);
-                *reinterpret_cast<__nv_bfloat162*>(orow + c + 2) = __floats2bfloat162_rn(0.f, 0.f);
-            }
-            if (lane == 0 && p.lse) p.lse[r * p.l_sr + h * p.l_sh] = -INFINITY;
-            continue;
-        }
-        float sum = 0.f;
-        for (int s = s0; s < s1; ++s) sum += expf(p.part_lse[(long long)s * p.H + h] - m);
-        const float lse = m + logf(sum);
-        for (int c = lane * 4; c < p.D; c += 128) {
-            float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int s = s0; s < s1; ++s) {
-                const float ls = p.part_lse[(long long)s * p.H + h];
-                if (ls == -INFINITY) continue;
-                const float w = expf(ls - lse);
-                const float4 v = *reinterpret_cast<const float4*>(p.part_o + ((long long)s * p.H + h) * p.D + c);
-                a.x += w * v.x;
-                a.y += w * v.y;
-                a.z += w * v.z;
-                a.w += w * v.w;
-            }
-            *reinterpret_cast<__nv_bfloat162*>(orow + c) = __floats2bfloat162_rn(a.x, a.y);
-            *reinterpret_cast<__nv_bfloat162*>(orow + c + 2) = __floats2bfloat162_rn(a.z, a.w);
-        }
-        if (lane == 0 && p.lse) p.lse[r * p.l_sr + h * p.l_sh] = lse;
+        warp_merge_head<0>(p.part_o, p.part_lse, p.H, s0, s1, h, p.o + r * p.o_sr, p.o_sh,
+                           p.lse ? p.lse + r * p.l_sr : nullptr, p.l_sh, lane, p.D);
     }
 }
 
@@ -604,8 +784,7 @@ int launch_merge(int32_t n_req, int32_t num_heads, int32_t head_dim, const int32
     int blocks = (pairs + 7) / 8;
     if (grid_hint > 0) blocks = std::min(blocks, grid_hint * 8);
     blocks = std::max(blocks, 1);
-    merge_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(p);
-    return int(cudaGetLastError());
+    return launch_pdl(merge_kernel, dim3(blocks), dim3(256), 0, stream, p);
 }
 
 // ============================================================================ plan device buffers
@@ -692,8 +871,7 @@ static int launch_decode_t(const spa_plan* P, const DecodeParams& dp, void* stre
     }
     const CUtensorMap* tk = reinterpret_cast<const CUtensorMap*>(P->pool->tmap_k.bytes);
     const CUtensorMap* tv = reinterpret_cast<const CUtensorMap*>(P->pool->tmap_v.bytes);
-    decode_kernel<D, MT><<<P->num_ctas, kWarps * 32, C::SMEM, static_cast<cudaStream_t>(stream)>>>(*tk, *tv, dp);
-    return int(cudaGetLastError());
+    return launch_pdl(decode_kernel<D, MT>, dim3(P->num_ctas), dim3(kWarps * 32), C::SMEM, stream, *tk, *tv, dp);
 }
 
 int launch_decode(const spa_plan* P, int32_t layer, const void* q, int64_t q_sr, int64_t q_sh, void* o, int64_t o_sr,
@@ -719,13 +897,14 @@ int launch_decode(const spa_plan* P, int32_t layer, const void* q, int64_t q_sr,
     dp.num_q_heads = c.num_q_heads;
     dp.num_kv_heads = c.num_kv_heads;
     dp.group_size = c.num_q_heads / c.num_kv_heads;
+    dp.fused_merge = P->cfg.fused_merge ? 1 : 0;
     int err = 0;
     if (c.head_dim == 64)
         err = P->mt == 1 ? launch_decode_t<64, 1>(P, dp, stream) : launch_decode_t<64, 2>(P, dp, stream);
     else
         err = P->mt == 1 ? launch_decode_t<128, 1>(P, dp, stream) : launch_decode_t<128, 2>(P, dp, stream);
     if (err) return err;
-    if (H[H_N_RECORDS] > 0)
+    if (H[H_N_RECORDS] > 0 && !dp.fused_merge)
         err = launch_merge(H[H_N_REQ], c.num_q_heads, c.head_dim, P->d_meta + H[H_OFF_REC_PTR], P->d_part_o,
                            P->d_part_lse, o, o_sr, o_sh, lse, l_sr, l_sh, P->num_ctas, stream);
     return err;

@@ -213,27 +213,11 @@ spa_status spa_decode_plan(spa_plan* P, int32_t n_req, const spa_req* reqs, int3
     std::vector<int32_t> order(n_items);
     std::iota(order.begin(), order.end(), 0);
     auto cost = [&](int32_t it) { return int64_t(descs[items[it].desc].n_pages) + 1; };
+    // dynamic LPT: the kernel's teams pop items from this queue (largest first) with one
+    // atomic each, so faster SMs take more work and the tail is made of the smallest items
     std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return cost(x) > cost(y); });
     const int T = P->n_teams;
-    std::vector<int32_t> owner(n_items);
-    {
-        using LT = std::pair<int64_t, int32_t>;
-        std::priority_queue<LT, std::vector<LT>, std::greater<LT>> heap;
-        for (int t = 0; t < T; ++t) heap.push({0, t});
-        for (int32_t it : order) {
-            LT top = heap.top();
-            heap.pop();
-            owner[it] = top.second;
-            heap.push({top.first + cost(it), top.second});
-        }
-    }
-    std::vector<int32_t> team_ptr(T + 1, 0), team_items(n_items);
-    for (int32_t it = 0; it < n_items; ++it) team_ptr[owner[it] + 1]++;
-    for (int t = 0; t < T; ++t) team_ptr[t + 1] += team_ptr[t];
-    {
-        std::vector<int32_t> fill(team_ptr.begin(), team_ptr.end() - 1);
-        for (int32_t it : order) team_items[fill[owner[it]]++] = it;   // largest first per team
-    }
+    const int32_t sched[4] = {0, 0, 0, 0};   // [0] next queue slot, [1] teams finished (self-resetting)
 
     // ---- 6. serialise: header + arrays (int32 words)
     std::vector<int32_t>& H = P->host;
@@ -247,10 +231,14 @@ spa_status spa_decode_plan(spa_plan* P, int32_t n_req, const spa_req* reqs, int3
     put(H_OFF_DESC, descs.data(), descs.size() * 8);
     put(H_OFF_MEMBER, members.data(), members.size() * 4);
     put(H_OFF_ITEM, items.data(), items.size() * 2);
-    put(H_OFF_TEAM_PTR, team_ptr.data(), team_ptr.size());
-    put(H_OFF_TEAM_ITEMS, team_items.data(), team_items.size());
+    put(H_OFF_SCHED, sched, 4);
+    put(H_OFF_QUEUE, order.data(), order.size());
     put(H_OFF_PAGES, pages.data(), pages.size());
     put(H_OFF_REC_PTR, rec_ptr.data(), rec_ptr.size());
+    {
+        const std::vector<int32_t> zeros(size_t(n_req) * Hkv, 0);
+        put(H_OFF_COUNTERS, zeros.data(), zeros.size());
+    }
     H[H_N_REQ] = n_req;
     H[H_N_DESC] = n_desc;
     H[H_N_ITEMS] = n_items;
@@ -301,8 +289,7 @@ spa_status spa_plan_debug_array(const spa_plan* plan, int32_t which, const int32
         case SPA_DBG_DESC: slot = H_OFF_DESC; width = 8; n = H[H_N_DESC]; break;
         case SPA_DBG_MEMBER: slot = H_OFF_MEMBER; width = 4; n = H[H_N_MEMBERS]; break;
         case SPA_DBG_ITEM: slot = H_OFF_ITEM; width = 2; n = H[H_N_ITEMS]; break;
-        case SPA_DBG_TEAM_PTR: slot = H_OFF_TEAM_PTR; n = H[H_N_TEAMS] + 1; break;
-        case SPA_DBG_TEAM_ITEMS: slot = H_OFF_TEAM_ITEMS; n = H[H_N_ITEMS]; break;
+        case SPA_DBG_QUEUE: slot = H_OFF_QUEUE; n = H[H_N_ITEMS]; break;
         case SPA_DBG_PAGES: slot = H_OFF_PAGES; n = H[H_N_PAGES]; break;
         case SPA_DBG_REC_PTR: slot = H_OFF_REC_PTR; n = H[H_N_REQ] + 1; break;
         default: return fail(SPA_ERR_INVALID_ARG, "unknown debug array");

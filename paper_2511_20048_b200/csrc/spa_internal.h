@@ -27,13 +27,14 @@ enum MetaHeader : int {
     H_OFF_DESC = 5,
     H_OFF_MEMBER = 6,
     H_OFF_ITEM = 7,
-    H_OFF_TEAM_PTR = 8,
-    H_OFF_TEAM_ITEMS = 9,
+    H_OFF_SCHED = 8,       // int32[4]: dynamic queue head, finished-team count (both reset in-kernel)
+    H_OFF_QUEUE = 9,       // int32[n_items]: item indices, largest first
     H_OFF_PAGES = 10,
     H_OFF_REC_PTR = 11,
     H_TOTAL = 12,
     H_N_MEMBERS = 13,
     H_N_PAGES = 14,
+    H_OFF_COUNTERS = 15,   // int32 [n_req][Hkv] arrival counters of the fused merge (zero between launches)
     H_WORDS = 16
 };
 

@@ -37,7 +37,8 @@ class spa_pool_config(ctypes.Structure):
 
 
 class spa_plan_config(ctypes.Structure):
-    _fields_ = [("sharing", c_int32), ("max_rows", c_int32), ("split_pages", c_int32), ("num_ctas", c_int32)]
+    _fields_ = [("sharing", c_int32), ("max_rows", c_int32), ("split_pages", c_int32), ("num_ctas", c_int32),
+                ("fused_merge", c_int32)]
 
 
 class spa_plan_stats(ctypes.Structure):
@@ -245,9 +246,9 @@ class Pool:
 
 
 class Plan:
-    def __init__(self, pool: Pool, sharing=True, max_rows=16, split_pages=0, num_ctas=0):
+    def __init__(self, pool: Pool, sharing=True, max_rows=16, split_pages=0, num_ctas=0, fused_merge=False):
         self.pool = pool
-        cfg = spa_plan_config(1 if sharing else 0, max_rows, split_pages, num_ctas)
+        cfg = spa_plan_config(1 if sharing else 0, max_rows, split_pages, num_ctas, 1 if fused_merge else 0)
         h = c_void_p()
         _check(lib().spa_plan_create(pool.h, ctypes.byref(cfg), ctypes.byref(h)))
         self.h = h

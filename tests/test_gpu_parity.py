@@ -109,11 +109,26 @@ def test_split_merge_equals_unsplit():
     rec = workloads.random_small(11, workloads.Model("m", 1, 8, 2, 128), max_prefix=400)
     e1, out1, *_ = run_parity(rec, "peaky", split_pages=1000)
     e2, out2, *_ = run_parity(rec, "peaky", split_pages=1)
+    e3, out3, *_ = run_parity(rec, "peaky", split_pages=1, fused_merge=True)
     _assert_ok(e1)
     _assert_ok(e2)
-    (o1, l1), (o2, l2) = out1[0], out2[0]
+    _assert_ok(e3)
+    (o1, l1), (o2, l2), (o3, l3) = out1[0], out2[0], out3[0]
     assert (o1.float() - o2.float()).abs().max().item() <= 8e-3
     assert (l1 - l2).abs().max().item() <= 1e-4
+    # the fused in-kernel merge and the standalone merge kernel compute the same sums
+    assert (o2.float() - o3.float()).abs().max().item() <= 4e-3
+    assert (l2 - l3).abs().max().item() <= 1e-5
+
+
+@pytest.mark.parametrize("fused", [False, True])
+@pytest.mark.parametrize("max_rows", [16, 32])
+def test_merge_paths_many_splits(fused, max_rows):
+    """Many splits per request, both merge paths, two layers (counters reset between launches)."""
+    rec = workloads.random_small(31, workloads.Model("m", 3, 16, 4, 128), max_prefix=500)
+    errs, *_ = run_parity(rec, "needle_shared_pos", split_pages=2, max_rows=max_rows, fused_merge=fused,
+                          num_ctas=9)
+    _assert_ok(errs)
 
 
 def test_deterministic_and_page_permutation_invariant():

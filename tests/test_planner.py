@@ -14,7 +14,7 @@ from paper_2511_20048_b200 import spa
 from paper_2511_20048_b200.spa import SpaError
 from spa_inputs import workloads
 
-DBG_DESC, DBG_MEMBER, DBG_ITEM, DBG_TEAM_PTR, DBG_TEAM_ITEMS, DBG_PAGES, DBG_REC_PTR = range(7)
+DBG_DESC, DBG_MEMBER, DBG_ITEM, DBG_QUEUE, _, DBG_PAGES, DBG_REC_PTR = range(7)
 
 
 def build(recipe, num_pages=None):
@@ -38,8 +38,7 @@ def check_plan(pool, plan, reqs, window):
     descs = plan.debug_array(DBG_DESC)
     mems = plan.debug_array(DBG_MEMBER)
     items = plan.debug_array(DBG_ITEM)
-    tptr = plan.debug_array(DBG_TEAM_PTR)
-    titems = plan.debug_array(DBG_TEAM_ITEMS)
+    queue = plan.debug_array(DBG_QUEUE)
     pages = plan.debug_array(DBG_PAGES)
     rec_ptr = plan.debug_array(DBG_REC_PTR)
     Hkv = pool.cfg.num_kv_heads
@@ -71,8 +70,10 @@ def check_plan(pool, plan, reqs, window):
             assert sorted(recs[r]) == list(range(rec_ptr[r], rec_ptr[r + 1]))
     assert len(items) == len(descs) * Hkv
     assert sorted((a, b) for a, b in items) == sorted((d, h) for d in range(len(descs)) for h in range(Hkv))
-    assert sorted(titems) == list(range(len(items)))
-    assert tptr[0] == 0 and tptr[-1] == len(items) and all(a <= b for a, b in zip(tptr, tptr[1:]))
+    assert sorted(queue) == list(range(len(items)))
+    costs = [descs[items[i][0]][1] for i in queue]
+    assert all(a >= b for a, b in zip(costs, costs[1:])), "queue must pop the largest items first"
+
     return descs, mems
 
 
@@ -167,7 +168,11 @@ def test_lpt_schedule_is_balanced():
     plan.plan(reqs)
     descs = plan.debug_array(DBG_DESC)
     items = plan.debug_array(DBG_ITEM)
-    tptr = plan.debug_array(DBG_TEAM_PTR)
-    titems = plan.debug_array(DBG_TEAM_ITEMS)
-    loads = [sum(descs[items[i][0]][1] + 1 for i in titems[a:b]) for a, b in zip(tptr, tptr[1:])]
+    queue = plan.debug_array(DBG_QUEUE)
+    import heapq
+    teams = [(0, t) for t in range(plan.stats()["n_teams"])]     # greedy list scheduling = the kernel's
+    for i in queue:                                              # dynamic queue at equal team speed
+        load, t = heapq.heappop(teams)
+        heapq.heappush(teams, (load + descs[items[i][0]][1] + 1, t))
+    loads = [l for l, _ in teams]
     assert max(loads) <= 1.15 * np.mean(loads)
