@@ -49,8 +49,8 @@ def parse():
                     help="cudaProfilerStart/Stop around the timed steps only (ncu --profile-from-start off); "
                          "skips parity, e2e and the cpu baseline")
     ap.add_argument("--sharing", type=int, default=1)
-    ap.add_argument("--fused-merge", action="store_true",
-                    help="merge split partials inside the decode kernel (default: PDL-chained merge kernel)")
+    ap.add_argument("--fused-merge", type=int, default=0,
+                    help="0: PDL-chained merge kernel, 1: last-arriver in-kernel merge, 2: in-kernel tail phase")
     ap.add_argument("--split-pages", type=int, default=0, help="max pages per split (0 = auto)")
     ap.add_argument("--layers", type=int, default=0, help="override resident layer count (0 = model's)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the oracle cpu_baseline sample")
@@ -376,6 +376,7 @@ def run_spa(args):
     alg_bytes = kv_bytes + qo_bytes + part_bytes
     pk, pk_kind = peaks()
     achieved = alg_bytes / (layer_ms * 1e-3) / 1e9
+    ceilings = spa.read_ceilings(pool) if not args.profile else None
 
     # ---- end-to-end through the public API with host buffers (pinned), copies inside
     e2e = None
@@ -416,7 +417,7 @@ def run_spa(args):
     if rank == 0:
         cpu = cpu_baseline(recipe, batch, args.cpu_seconds) if world == 1 and not args.profile else None
         ck = clocks.summary(local)
-        sep = (not args.fused_merge) and st["n_records"] > 0
+        sep = args.fused_merge == 0 and st["n_records"] > 0
         launches_per_step = (-(-N // 896)) + L * (2 if sep else 1)
         result = {
             "metric": METRIC,
@@ -445,7 +446,9 @@ def run_spa(args):
                          "kernel": ("decode_kernel + merge_kernel (one spa_decode_attention call)" if sep
                                     else "decode_kernel (split merge fused in-kernel)"),
                          "peak_kind": pk_kind, "alg_bytes_per_launch": int(alg_bytes),
-                         "frac_of_8tbs": achieved / 8000.0},
+                         "frac_of_8tbs": achieved / 8000.0,
+                         "same_run_read_ceilings_gbs": ceilings,
+                         "frac_of_tma_ceiling": (achieved / ceilings["tma_pool_read_gbs"]) if ceilings else None},
             "sharing": {"unique_tokens_per_kv_head": st["unique_tokens"],
                         "unshared_tokens_per_kv_head": st["unshared_tokens"],
                         "bytes_vs_unshared": st["unique_tokens"] / st["unshared_tokens"]},

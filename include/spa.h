@@ -131,7 +131,8 @@ typedef struct spa_plan_config {
     int32_t fused_merge;    /* 0 (default): split partials are merged by a merge_kernel launched
                                right after the decode kernel (programmatic dependent launch);
                                1: inside the decode kernel by the last item of each (request, KV
-                               head).  spa_merge_splits semantics either way.                    */
+                               head); 2: inside the decode kernel, by teams that found the work
+                               queue empty (tail phase).  spa_merge_splits semantics always.     */
 } spa_plan_config;
 
 /* cfg may be NULL (defaults).  The plan keeps a pointer to `pool`. */

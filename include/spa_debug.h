@@ -5,7 +5,8 @@
  * Views stay valid until the next spa_decode_plan / spa_plan_destroy on the plan.
  *
  *   SPA_DBG_DESC      rows of 8: page_off, n_pages, tok_start, tok_end, member_off,
- *                     n_members, kind (0 shared, 1 tail), group
+ *                     n_members, kind (bit 0: member tail, else shared; bit 2: holds a
+ *                     member's newest token), group
  *                     -> keys [tok_start, tok_end) read through pages[page_off ..+n_pages)
  *   SPA_DBG_MEMBER    rows of 4: batch row, window lower bound lo, record (-1 = direct
  *                     output), reserved
@@ -35,6 +36,18 @@ enum {
 
 spa_status spa_plan_debug_array(const spa_plan* plan, int32_t which, const int32_t** out_data,
                                 int64_t* out_len, int32_t* out_row_width);
+
+/* Read-bandwidth probes (bench.py reports them as same-run ceilings next to the decode
+ * kernel's achieved bandwidth).  Asynchronous on `stream`; time them with events.
+ *   spa_debug_read_bw_ldg:   streaming 16-B loads over `bytes` of device memory at `buf`;
+ *                            sink4 = 4 bytes of device scratch.
+ *   spa_debug_pool_read_tma: the decode kernel's TMA/mbarrier pipeline without the math,
+ *                            over every page and KV head of layers [0, layers) of both pools;
+ *                            mode 0: 2-D 64x16 boxes (as the decode kernel), 1: 3-D
+ *                            64x(d/64)x16 boxes, 2: 1-D cp.async.bulk of each 4 KB page-head.
+ * Bytes read by the TMA probe: layers * (num_pages / 2 * 2) * Hkv * page_size * d * 2 * 2. */
+spa_status spa_debug_read_bw_ldg(const void* buf, size_t bytes, void* sink4, void* stream);
+spa_status spa_debug_pool_read_tma(const spa_pool* pool, int32_t layers, int32_t mode, void* stream);
 
 #ifdef __cplusplus
 }

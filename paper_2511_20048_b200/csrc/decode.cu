@@ -1,0 +1,622 @@
+// a5: the shared-prefix paged GQA decode-attention kernel (sm_100a) and its launcher.
+//
+// Persistent grid: one CTA of 8 warps per SM.  A TEAM of MT x KW warps owns a private
+// shared-memory ring of NS stages; each stage holds PPS pages of K and V for one KV head,
+// brought in by ONE 3-D TMA box per (page, head) and tensor, completing on an mbarrier.
+// Teams pop work items (descriptor, KV head) from a dynamic longest-first queue.  An item
+// carries every query row of a request group (R = members x G <= 16 MT), so the pages of
+// a shared agent context c_i are read from HBM once per (KV head, group) for the main
+// request and all its speculative forks (north_star).
+//   wt (0..MT-1)  which 16-row tile of the item's query rows a warp computes
+//   wk (0..KW-1)  which pages of each stage a warp consumes (page j -> warp j % KW); the KW
+//                 partial softmax states of a row tile are combined through shared memory
+//                 at the end of the item (flash-decoding inside the team).
+// QK^T and PV are mma.sync.m16n8k16 bf16 tiles (fp32 accumulate) fed by ldmatrix from the
+// 128-B-swizzled tiles; the online softmax runs in the log2 domain with lazy rescaling.
+// Each item writes either the final O (bf16) / LSE (fp32) of its rows or an fp32 partial
+// record; partials are merged by the merge kernel (or in-kernel, fused_merge = 1 / 2).
+#include <cstdlib>
+
+#include "device_util.cuh"
+#include "spa_internal.h"
+
+namespace spa {
+
+int launch_merge(int32_t n_req, int32_t num_heads, int32_t head_dim, const int32_t* rec_ptr, const float* part_o,
+                 const float* part_lse, void* o, int64_t o_sr, int64_t o_sh, float* lse, int64_t l_sr, int64_t l_sh,
+                 int grid_hint, void* stream);
+
+struct DecodeParams {
+    const int32_t* meta;
+    const __nv_bfloat16* q;
+    long long q_sr, q_sh;
+    __nv_bfloat16* o;
+    long long o_sr, o_sh;
+    float* lse;
+    long long l_sr, l_sh;
+    float* part_o;
+    float* part_lse;
+    float scale_log2;
+    int layer_row_base;  // layer * num_pages * Hkv * 16
+    int num_q_heads, group_size, num_kv_heads;
+    int fused_merge;     // 0 merge kernel, 1 last arriver merges, 2 tail phase merges
+    int layer;           // selects this launch's work-queue counters
+};
+
+constexpr int kDecodeWarps = 8;
+constexpr int kSmemMax = 232448;   // 227 KB: the sm_100 per-block dynamic shared memory limit
+
+template <int D, int MT, int PPS>
+struct DecodeCfg {
+    static constexpr int KW = 2;                          // key-split warps per row tile
+    static constexpr int TEAM_WARPS = MT * KW;
+    static constexpr int TEAMS = kDecodeWarps / TEAM_WARPS;
+    static constexpr int PAGE_BYTES = kPageSize * D * 2;  // K (or V) of one page, one head
+    static constexpr int STAGE_BYTES = PPS * 2 * PAGE_BYTES;
+    // per (team, row tile): column-half exchange [2][16][D/2] fp32 + (m, l) [2][16][2]
+    static constexpr int COMB_BYTES = TEAMS * MT * (2 * 16 * (D / 2) * 4 + 2 * 16 * 2 * 4);
+    // barriers (full + empty), the team mailbox and the popped-item queue, for n stages
+    static constexpr int misc(int n) { return TEAMS * n * 2 * 8 + TEAMS * 4 + TEAMS * (n + 2) * 4 + 16; }
+    static constexpr int max_stages() {
+        int n = 1;
+        while (1024 + (n + 1) * TEAMS * STAGE_BYTES + misc(n + 1) + COMB_BYTES <= kSmemMax) ++n;
+        return n;
+    }
+    static constexpr int NS = max_stages();
+    static constexpr int MISC_BYTES = misc(NS);
+    static constexpr int RING_BYTES = TEAMS * NS * STAGE_BYTES;
+    static constexpr int QN = NS + 2;                     // popped-item queue entries per team
+    static constexpr int OFF_BARS = RING_BYTES;
+    static constexpr int OFF_SLOT = OFF_BARS + TEAMS * NS * 2 * 8;
+    static constexpr int OFF_TQ = OFF_SLOT + TEAMS * 4;
+    static constexpr int OFF_COMB = (OFF_TQ + TEAMS * QN * 4 + 15) & ~15;
+    static constexpr int SMEM = 1024 + OFF_COMB + COMB_BYTES;
+    static_assert(NS >= 2, "pipeline needs >= 2 stages");
+    static_assert(PPS % KW == 0, "each key-split warp takes whole pages");
+    static_assert(OFF_COMB - OFF_BARS <= MISC_BYTES, "misc shared-memory region too small");
+    static_assert(SMEM <= kSmemMax, "shared memory over the sm_100 limit");
+};
+
+template <int D, int MT, int PPS>
+__global__ void __launch_bounds__(kDecodeWarps * 32, 1)
+    decode_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
+                  const DecodeParams p) {
+    using C = DecodeCfg<D, MT, PPS>;
+    constexpr int KW = C::KW;
+    constexpr int JW = PPS / KW;   // pages per warp per stage
+    constexpr int KS = D / 16;     // k16 steps over the head dimension
+    constexpr int NT = D / 8;      // n8 tiles of the output
+    constexpr int NTH = NT / 2;    // n8 tiles per column half
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+
+    const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0);   // provably warp-uniform
+    const int lane = threadIdx.x & 31;
+    const int team = warp / C::TEAM_WARPS;
+    const int tw = warp - team * C::TEAM_WARPS;
+    const int wt = tw / KW, wk = tw - (tw / KW) * KW;
+    const bool producer = tw == 0;
+    const uint32_t ring = smem_u32(smem) + team * C::NS * C::STAGE_BYTES;
+    const uint32_t bars = smem_u32(smem) + C::OFF_BARS;
+    auto full_bar = [&](int s) { return bars + (team * C::NS + s) * 8; };
+    auto empty_bar = [&](int s) { return bars + (C::TEAMS * C::NS + team * C::NS + s) * 8; };
+    uint32_t* team_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_SLOT) + team;
+    int32_t* tq = reinterpret_cast<int32_t*>(smem + C::OFF_TQ) + team * C::QN;
+    float* comb = reinterpret_cast<float*>(smem + C::OFF_COMB) + (team * MT + wt) * (2 * 16 * (D / 2) + 2 * 16 * 2);
+    float* ml = comb + 2 * 16 * (D / 2);
+    auto team_sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(C::TEAM_WARPS * 32) : "memory"); };
+    auto pair_sync = [&]() {
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + C::TEAMS + team * MT + wt), "r"(KW * 32) : "memory");
+    };
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < C::TEAMS * C::NS; ++i) {
+            mbar_init(bars + i * 8, 1);
+            mbar_init(bars + (C::TEAMS * C::NS + i) * 8, C::TEAM_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // Programmatic dependent launch: this kernel may start while the previous kernel on the
+    // stream (the previous layer's decode / merge) drains.  Until griddepcontrol.wait it
+    // only reads what earlier stream work wrote (plan, KV pages other than the newest token
+    // of each request) and its own layer's queue counters; queries, outputs, partials and
+    // merge counters are touched after the wait.
+    asm volatile("griddepcontrol.launch_dependents;");
+
+    const int32_t* meta = p.meta;
+    const Desc* descs = reinterpret_cast<const Desc*>(meta + meta[H_OFF_DESC]);
+    const Member* mems = reinterpret_cast<const Member*>(meta + meta[H_OFF_MEMBER]);
+    const Item* items = reinterpret_cast<const Item*>(meta + meta[H_OFF_ITEM]);
+    const int32_t* queue = meta + meta[H_OFF_QUEUE];
+    const int32_t* pages = meta + meta[H_OFF_PAGES];
+    const int32_t* rec_ptr = meta + meta[H_OFF_REC_PTR];
+    int32_t* counters = const_cast<int32_t*>(meta) + meta[H_OFF_COUNTERS];
+    int32_t* sched = const_cast<int32_t*>(meta) + meta[H_OFF_SCHED] + 4 * p.layer;
+    const int n_items = meta[H_N_ITEMS];
+    const int G = p.group_size, Hq = p.num_q_heads, Hkv = p.num_kv_heads;
+    uint64_t policy = 0;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+
+    // ---- producer (warp tw == 0 of the team, warp-collective; lane 0 issues): pops items
+    //      from the dynamic queue and streams their stages NS ahead.  Page ids come from a
+    //      two-block register cache (lane i holds page base+i and base+32+i) so the global
+    //      page-list loads stay off the critical path.  TMA operands are broadcast from
+    //      lane 0 (warp-uniform).  Queue empty: publish -1, complete the barrier without data.
+    int p_item = -1, p_st = 0, p_n = 0;
+    bool p_done = false, p_waited = false;
+    int p_kv = 0, p_npages = 0, p_off = 0;
+    int pid_base = 0, pid_cur = 0, pid_next = 0;
+    auto issue_next = [&](int slot) {
+        if (p_done) return;
+        if (p_item < 0) {
+            int qi = 0;
+            if (lane == 0) qi = atomicAdd(sched, 1);
+            qi = __shfl_sync(0xffffffffu, qi, 0);
+            const int it = qi < n_items ? queue[qi] : -1;
+            if (lane == 0) tq[p_n % C::QN] = it;
+            ++p_n;
+            if (it < 0) {
+                p_done = true;
+                if (lane == 0) mbar_arrive(full_bar(slot));
+                return;
+            }
+            p_item = it;
+            p_st = 0;
+            const Item itm = items[it];
+            const Desc dsc = descs[itm.desc];
+            if ((dsc.kind & 4) && !p_waited) {   // holds a newest token: wait for its producer
+                asm volatile("griddepcontrol.wait;" ::: "memory");
+                p_waited = true;
+            }
+            p_kv = itm.kv_head;
+            p_npages = dsc.n_pages;
+            p_off = dsc.page_off;
+            pid_base = 0;
+            pid_cur = lane < p_npages ? pages[p_off + lane] : 0;
+            pid_next = 32 + lane < p_npages ? pages[p_off + 32 + lane] : 0;
+        }
+        const int p0 = p_st * PPS;
+        const int npg = min(PPS, p_npages - p0);
+        int row[PPS];
+#pragma unroll
+        for (int j = 0; j < PPS; ++j) {
+            const int k = p0 + j;
+            if (k >= pid_base + 32) {   // sequential: step to the next block, prefetch the one after
+                pid_base += 32;
+                pid_cur = pid_next;
+                const int kk = pid_base + 32 + lane;
+                pid_next = kk < p_npages ? pages[p_off + kk] : 0;
+            }
+            const int page = __shfl_sync(0xffffffffu, pid_cur, (k - pid_base) & 31);
+            row[j] = __shfl_sync(0xffffffffu, p.layer_row_base + (page * Hkv + p_kv) * kPageSize, 0);
+        }
+        if (lane == 0) {
+            const uint32_t fb = full_bar(slot);
+            mbar_expect_tx(fb, npg * 2 * C::PAGE_BYTES);
+            const uint32_t sb = ring + slot * C::STAGE_BYTES;
+#pragma unroll
+            for (int j = 0; j < PPS; ++j) {
+                if (j < npg) {
+                    tma_load_3d(sb + j * 2 * C::PAGE_BYTES, &tmk, 0, row[j], 0, fb, policy);
+                    tma_load_3d(sb + j * 2 * C::PAGE_BYTES + C::PAGE_BYTES, &tmv, 0, row[j], 0, fb, policy);
+                }
+            }
+        }
+        __syncwarp();
+        if (++p_st * PPS >= p_npages) p_item = -1;
+    };
+    if (producer) {
+        for (int s = 0; s < C::NS; ++s) issue_next(s);
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+
+    int slot = 0, c_n = 0;
+    uint32_t phase = 0;
+    while (true) {
+        // the first stage of the next item (or the end-of-queue marker) has landed
+        mbar_wait(full_bar(slot), phase);
+        const int it = tq[c_n % C::QN];
+        ++c_n;
+        if (it < 0) break;
+        const Item itm = items[it];
+        const Desc dsc = descs[itm.desc];
+        const int R = dsc.n_members * G;
+        const bool active = wt * 16 < R;   // identical for the KW warps of a row tile
+        const int row0 = wt * 16 + (lane >> 2), row1 = row0 + 8;
+
+        // ---- per-row setup: member, window bound, query fragments (padding rows: q = 0, lo = 0)
+        int lo0 = 0, lo1 = 0;
+        uint32_t qa[KS][4];
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) qa[ks][0] = qa[ks][1] = qa[ks][2] = qa[ks][3] = 0u;
+        if (active) {
+            const __nv_bfloat16* q0 = nullptr;
+            const __nv_bfloat16* q1 = nullptr;
+            if (row0 < R) {
+                const int mb = row0 / G;
+                const Member m = mems[dsc.member_off + mb];
+                lo0 = m.lo;
+                q0 = p.q + m.row * p.q_sr + (itm.kv_head * G + row0 - mb * G) * p.q_sh;
+            }
+            if (row1 < R) {
+                const int mb = row1 / G;
+                const Member m = mems[dsc.member_off + mb];
+                lo1 = m.lo;
+                q1 = p.q + m.row * p.q_sr + (itm.kv_head * G + row1 - mb * G) * p.q_sh;
+            }
+            const int cq = 2 * (lane & 3);
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) {
+                if (q0) {
+                    qa[ks][0] = *reinterpret_cast<const uint32_t*>(q0 + ks * 16 + cq);
+                    qa[ks][2] = *reinterpret_cast<const uint32_t*>(q0 + ks * 16 + cq + 8);
+                }
+                if (q1) {
+                    qa[ks][1] = *reinterpret_cast<const uint32_t*>(q1 + ks * 16 + cq);
+                    qa[ks][3] = *reinterpret_cast<const uint32_t*>(q1 + ks * 16 + cq + 8);
+                }
+            }
+        }
+        // keys >= lo_warp are inside every row's window: such pages need no window mask
+        int lo_warp = max(lo0, lo1);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) lo_warp = max(lo_warp, __shfl_xor_sync(0xffffffffu, lo_warp, o));
+        // running max per row, log2 units, raised lazily (only when a page's max exceeds it
+        // by > kRescale, so P <= 2^kRescale); the same m is used for P, l and the LSE.
+        constexpr float kRescale = 8.f;
+        float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+        float acc[NT][4];
+#pragma unroll
+        for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
+
+        const int nst = (dsc.n_pages + PPS - 1) / PPS;
+        for (int st = 0; st < nst; ++st) {
+            if (st > 0) mbar_wait(full_bar(slot), phase);
+            const int npg = min(PPS, dsc.n_pages - st * PPS);
+            if (active) {
+                const uint32_t sb = ring + slot * C::STAGE_BYTES;
+                float s[JW][2][4];
+#pragma unroll
+                for (int jj = 0; jj < JW; ++jj) {
+                    const int j = wk + jj * KW;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) s[jj][0][e] = s[jj][1][e] = 0.f;
+                    if (j < npg) {
+                        const uint32_t kb = sb + j * 2 * C::PAGE_BYTES;
+                        const int key = ((lane >> 4) << 3) + (lane & 7);
+#pragma unroll
+                        for (int ks = 0; ks < KS; ++ks) {
+                            const int dcol = ks * 16 + ((lane >> 3) & 1) * 8;
+                            const uint32_t addr =
+                                kb + (dcol >> 6) * 2048 + key * 128 + ((((dcol & 63) >> 3) ^ (key & 7)) << 4);
+                            uint32_t b0, b1, b2, b3;
+                            ldsm_x4(b0, b1, b2, b3, addr);
+                            mma16816(s[jj][0], qa[ks], b0, b1);
+                            mma16816(s[jj][1], qa[ks], b2, b3);
+                        }
+                    }
+                }
+                // mask + scale (log2 domain), row max over this warp's pages
+                float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+                for (int jj = 0; jj < JW; ++jj) {
+                    const int j = wk + jj * KW;
+                    const int tokp = dsc.tok_start + (st * PPS + j) * kPageSize;
+                    const bool unmasked = (j < npg) && (tokp >= lo_warp) && (tokp + kPageSize <= dsc.tok_end);
+                    if (unmasked) {
+#pragma unroll
+                        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const float v = s[jj][nt][e] * p.scale_log2;
+                                s[jj][nt][e] = v;
+                                if (e < 2) mx0 = fmaxf(mx0, v);
+                                else mx1 = fmaxf(mx1, v);
+                            }
+                    } else {
+#pragma unroll
+                        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const int tok = tokp + nt * 8 + 2 * (lane & 3) + (e & 1);
+                                const int lo = (e < 2) ? lo0 : lo1;
+                                const bool ok = (j < npg) && (tok < dsc.tok_end) && (tok >= lo);
+                                const float v = ok ? s[jj][nt][e] * p.scale_log2 : -INFINITY;
+                                s[jj][nt][e] = v;
+                                if (e < 2) mx0 = fmaxf(mx0, v);
+                                else mx1 = fmaxf(mx1, v);
+                            }
+                    }
+                }
+                mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+                mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+                mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+                mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+                // -inf - -inf would be NaN: (m == -inf) means "no live key yet"
+                const bool grow = (mx0 > m0 + kRescale) || (mx1 > m1 + kRescale) ||
+                                  (m0 == -INFINITY && mx0 > -INFINITY) || (m1 == -INFINITY && mx1 > -INFINITY);
+                if (__any_sync(0xffffffffu, grow)) {
+                    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+                    const float al0 = (m0 == -INFINITY) ? 0.f : fast_exp2(m0 - mn0);
+                    const float al1 = (m1 == -INFINITY) ? 0.f : fast_exp2(m1 - mn1);
+                    m0 = mn0;
+                    m1 = mn1;
+                    l0 *= al0;
+                    l1 *= al1;
+#pragma unroll
+                    for (int n = 0; n < NT; ++n) {
+                        acc[n][0] *= al0;
+                        acc[n][1] *= al0;
+                        acc[n][2] *= al1;
+                        acc[n][3] *= al1;
+                    }
+                }
+                const float mu0 = (m0 == -INFINITY) ? 0.f : m0;
+                const float mu1 = (m1 == -INFINITY) ? 0.f : m1;
+                // P = exp2(s - m): l accumulates the fp32 P (the LSE carries no bf16 rounding);
+                // the PV MMA takes P rounded to bf16 (A fragments).
+#pragma unroll
+                for (int jj = 0; jj < JW; ++jj) {
+                    const int j = wk + jj * KW;
+                    if (j < npg) {
+                        float e[2][4];
+#pragma unroll
+                        for (int nt = 0; nt < 2; ++nt) {
+                            e[nt][0] = fast_exp2(s[jj][nt][0] - mu0);
+                            e[nt][1] = fast_exp2(s[jj][nt][1] - mu0);
+                            e[nt][2] = fast_exp2(s[jj][nt][2] - mu1);
+                            e[nt][3] = fast_exp2(s[jj][nt][3] - mu1);
+                            l0 += e[nt][0] + e[nt][1];
+                            l1 += e[nt][2] + e[nt][3];
+                        }
+                        uint32_t pa[4];
+                        pa[0] = pack_bf16(e[0][0], e[0][1]);
+                        pa[1] = pack_bf16(e[0][2], e[0][3]);
+                        pa[2] = pack_bf16(e[1][0], e[1][1]);
+                        pa[3] = pack_bf16(e[1][2], e[1][3]);
+                        const uint32_t vb = sb + j * 2 * C::PAGE_BYTES + C::PAGE_BYTES;
+                        const int key = (((lane >> 3) & 1) << 3) + (lane & 7);
+#pragma unroll
+                        for (int dn = 0; dn < KS; ++dn) {
+                            const int dchunk = 2 * dn + (lane >> 4);
+                            const uint32_t addr = vb + (dchunk >> 3) * 2048 + key * 128 + (((dchunk & 7) ^ (key & 7)) << 4);
+                            uint32_t b0, b1, b2, b3;
+                            ldsm_x4_t(b0, b1, b2, b3, addr);
+                            mma16816(acc[2 * dn], pa, b0, b1);
+                            mma16816(acc[2 * dn + 1], pa, b2, b3);
+                        }
+                    }
+                }
+            }
+            // ---- release the stage; the producer refills it NS stages ahead
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty_bar(slot));
+            if (producer) {
+                mbar_wait(empty_bar(slot), phase);
+                issue_next(slot);
+            }
+            if (++slot == C::NS) {
+                slot = 0;
+                phase ^= 1u;
+            }
+        }
+
+        // ---- epilogue: combine the KW key-split states of each row tile, normalise, and
+        //      write each column half (warp wk owns columns [wk D/2, (wk+1) D/2)).
+        if (active) {
+            l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+            l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+            l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+            l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+            const int r0 = lane >> 2, c0 = 2 * (lane & 3);
+            // publish (m, l) and the OTHER warp's column half of the unscaled accumulator
+            if ((lane & 3) == 0) {
+                ml[(wk * 16 + r0) * 2 + 0] = m0;
+                ml[(wk * 16 + r0) * 2 + 1] = l0;
+                ml[(wk * 16 + r0 + 8) * 2 + 0] = m1;
+                ml[(wk * 16 + r0 + 8) * 2 + 1] = l1;
+            }
+            // (register arrays need compile-time indices: one branch per key-split warp)
+            auto publish = [&](float* dst, const float (*a)[4]) {
+#pragma unroll
+                for (int n = 0; n < NTH; ++n) {
+                    const int col = n * 8 + c0;
+                    *reinterpret_cast<float2*>(dst + r0 * (D / 2) + col) = make_float2(a[n][0], a[n][1]);
+                    *reinterpret_cast<float2*>(dst + (r0 + 8) * (D / 2) + col) = make_float2(a[n][2], a[n][3]);
+                }
+            };
+            if (wk == 0) publish(comb + 16 * (D / 2), acc + NTH);
+            else publish(comb, acc);
+            pair_sync();
+            const int ow = 1 - wk;
+            const float om0 = ml[(ow * 16 + r0) * 2 + 0], ol0 = ml[(ow * 16 + r0) * 2 + 1];
+            const float om1 = ml[(ow * 16 + r0 + 8) * 2 + 0], ol1 = ml[(ow * 16 + r0 + 8) * 2 + 1];
+            const float mt0 = fmaxf(m0, om0), mt1 = fmaxf(m1, om1);
+            const float sa0 = m0 == -INFINITY ? 0.f : fast_exp2(m0 - mt0);
+            const float sb0 = om0 == -INFINITY ? 0.f : fast_exp2(om0 - mt0);
+            const float sa1 = m1 == -INFINITY ? 0.f : fast_exp2(m1 - mt1);
+            const float sb1 = om1 == -INFINITY ? 0.f : fast_exp2(om1 - mt1);
+            const float lt0 = l0 * sa0 + ol0 * sb0, lt1 = l1 * sa1 + ol1 * sb1;
+            float half[NTH][4];
+            auto gather = [&](const float* src, const float (*a)[4]) {
+#pragma unroll
+                for (int n = 0; n < NTH; ++n) {
+                    const int col = n * 8 + c0;
+                    const float2 x = *reinterpret_cast<const float2*>(src + r0 * (D / 2) + col);
+                    const float2 y = *reinterpret_cast<const float2*>(src + (r0 + 8) * (D / 2) + col);
+                    half[n][0] = a[n][0] * sa0 + x.x * sb0;
+                    half[n][1] = a[n][1] * sa0 + x.y * sb0;
+                    half[n][2] = a[n][2] * sa1 + y.x * sb1;
+                    half[n][3] = a[n][3] * sa1 + y.y * sb1;
+                }
+            };
+            if (wk == 0) gather(comb, acc);
+            else gather(comb + 16 * (D / 2), acc + NTH);
+            pair_sync();   // the exchange buffers may be rewritten by the next item
+#pragma unroll
+            for (int rr = 0; rr < 2; ++rr) {
+                const int row = rr ? row1 : row0;
+                if (row < R) {
+                    const int mb = row / G;
+                    const Member m = mems[dsc.member_off + mb];
+                    const int head = itm.kv_head * G + (row - mb * G);
+                    const float l = rr ? lt1 : lt0;
+                    const float mm = rr ? mt1 : mt0;
+                    const float inv = l > 0.f ? 1.f / l : 0.f;
+                    const float lse = l > 0.f ? (mm + log2f(l)) * 0.69314718055994531f : -INFINITY;
+                    if (m.rec < 0) {
+                        __nv_bfloat16* orow = p.o + m.row * p.o_sr + head * p.o_sh + wk * (D / 2);
+#pragma unroll
+                        for (int n = 0; n < NTH; ++n)
+                            *reinterpret_cast<__nv_bfloat162*>(orow + n * 8 + c0) =
+                                __floats2bfloat162_rn(half[n][2 * rr] * inv, half[n][2 * rr + 1] * inv);
+                        if ((lane & 3) == 0 && wk == 0 && p.lse) p.lse[m.row * p.l_sr + head * p.l_sh] = lse;
+                    } else {
+                        float* prow = p.part_o + ((long long)m.rec * Hq + head) * D + wk * (D / 2);
+#pragma unroll
+                        for (int n = 0; n < NTH; ++n)
+                            *reinterpret_cast<float2*>(prow + n * 8 + c0) =
+                                make_float2(half[n][2 * rr] * inv, half[n][2 * rr + 1] * inv);
+                        if ((lane & 3) == 0 && wk == 0) p.part_lse[(long long)m.rec * Hq + head] = lse;
+                    }
+                }
+            }
+        }
+
+        // ---- in-kernel split merge (fused_merge 1 / 2)
+        bool any_partial = false;
+        for (int mb = 0; mb < dsc.n_members; ++mb) any_partial |= mems[dsc.member_off + mb].rec >= 0;
+        if (any_partial && p.fused_merge == 2) {
+            // tail merge: count this item's records in (release); merged after the queue
+            team_sync();
+            if (producer && lane == 0)
+                for (int mb = 0; mb < dsc.n_members; ++mb) {
+                    const Member mm = mems[dsc.member_off + mb];
+                    if (mm.rec >= 0) red_add_release_gpu(counters + mm.row * Hkv + itm.kv_head, 1);
+                }
+        } else if (any_partial && p.fused_merge == 1) {
+            // the team barrier orders every lane's partial stores before the producer lane's
+            // acq_rel arrival (release is cumulative); the last arriver acquires all of them
+            team_sync();
+            uint32_t mask = 0;
+            if (producer && lane == 0) {
+                for (int mb = 0; mb < dsc.n_members; ++mb) {
+                    const Member mm = mems[dsc.member_off + mb];
+                    if (mm.rec < 0) continue;
+                    const int nrec = rec_ptr[mm.row + 1] - rec_ptr[mm.row];
+                    int* c = counters + mm.row * Hkv + itm.kv_head;
+                    if (atom_add_acq_rel_gpu(c, 1) == nrec - 1) {
+                        mask |= 1u << mb;
+                        *c = 0;    // every arrival of this launch is in: ready for the next layer
+                    }
+                }
+                *team_slot = mask;
+            }
+            team_sync();
+            mask = *team_slot;
+            team_sync();
+            while (mask) {
+                const int mb = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const Member mm = mems[dsc.member_off + mb];
+                for (int hh = tw; hh < G; hh += C::TEAM_WARPS)
+                    warp_merge_head<D>(p.part_o, p.part_lse, Hq, rec_ptr[mm.row], rec_ptr[mm.row + 1],
+                                       itm.kv_head * G + hh, p.o + mm.row * p.o_sr, p.o_sh,
+                                       p.lse ? p.lse + mm.row * p.l_sr : nullptr, p.l_sh, lane);
+            }
+        }
+    }
+
+    // ---- tail merge (fused_merge == 2): every item has been popped; teams now pop merge
+    //      tasks (request, KV head), wait until all of the task's records are counted in
+    //      (acquire; the items still running are owned by teams not in this loop), merge.
+    if (p.fused_merge == 2) {
+        const int32_t* mtask = meta + meta[H_OFF_MTASK];
+        const int n_mtask = meta[H_N_MTASK];
+        while (true) {
+            team_sync();
+            if (producer && lane == 0) *team_slot = uint32_t(atomicAdd(sched + 2, 1));
+            team_sync();
+            const int t = int(*team_slot);
+            if (t >= n_mtask) break;
+            const int task = mtask[t];
+            const int row = task / Hkv, g = task - row * Hkv;
+            const int s0 = rec_ptr[row], s1 = rec_ptr[row + 1];
+            if (producer && lane == 0) {
+                int* c = counters + task;
+                while (ld_acquire_gpu(c) < s1 - s0) __nanosleep(64);
+                *c = 0;   // all arrivals of this launch are in
+            }
+            team_sync();
+            for (int hh = tw; hh < G; hh += C::TEAM_WARPS)
+                warp_merge_head<D>(p.part_o, p.part_lse, Hq, s0, s1, g * G + hh, p.o + row * p.o_sr, p.o_sh,
+                                   p.lse ? p.lse + row * p.l_sr : nullptr, p.l_sh, lane);
+        }
+    }
+    // the last team to finish rewinds the queues for the next launch (stream-ordered)
+    if (producer && lane == 0) {
+        if (atomicAdd(sched + 1, 1) == int(gridDim.x) * C::TEAMS - 1) {
+            sched[0] = 0;
+            sched[1] = 0;
+            sched[2] = 0;
+        }
+    }
+}
+
+template <int D, int MT, int PPS>
+static int launch_decode_t(const spa_plan* P, const DecodeParams& dp, void* stream) {
+    using C = DecodeCfg<D, MT, PPS>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e =
+            cudaFuncSetAttribute(decode_kernel<D, MT, PPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        if (e) return int(e);
+        attr_set = true;
+    }
+    const CUtensorMap* tk = reinterpret_cast<const CUtensorMap*>(P->pool->tmap_k.bytes);
+    const CUtensorMap* tv = reinterpret_cast<const CUtensorMap*>(P->pool->tmap_v.bytes);
+    return launch_pdl(decode_kernel<D, MT, PPS>, dim3(P->num_ctas), dim3(kDecodeWarps * 32), C::SMEM, stream, *tk,
+                      *tv, dp);
+}
+
+int decode_teams_per_cta(int mt) { return kDecodeWarps / (mt * 2); }
+
+int launch_decode(const spa_plan* P, int32_t layer, const void* q, int64_t q_sr, int64_t q_sh, void* o, int64_t o_sr,
+                  int64_t o_sh, float* lse, int64_t l_sr, int64_t l_sh, float scale, void* stream) {
+    const auto& c = P->pool->cfg;
+    const int32_t* H = P->host.data();
+    if (H[H_N_ITEMS] == 0) return 0;
+    DecodeParams dp{};
+    dp.meta = P->d_meta;
+    dp.q = static_cast<const __nv_bfloat16*>(q);
+    dp.q_sr = q_sr;
+    dp.q_sh = q_sh;
+    dp.o = static_cast<__nv_bfloat16*>(o);
+    dp.o_sr = o_sr;
+    dp.o_sh = o_sh;
+    dp.lse = lse;
+    dp.l_sr = l_sr;
+    dp.l_sh = l_sh;
+    dp.part_o = P->d_part_o;
+    dp.part_lse = P->d_part_lse;
+    dp.scale_log2 = float(double(scale) * 1.4426950408889634);
+    dp.layer_row_base = layer * c.num_pages * c.num_kv_heads * kPageSize;
+    dp.num_q_heads = c.num_q_heads;
+    dp.num_kv_heads = c.num_kv_heads;
+    dp.group_size = c.num_q_heads / c.num_kv_heads;
+    dp.fused_merge = P->cfg.fused_merge;
+    dp.layer = layer;
+    int err = 0;
+    if (c.head_dim == 64)
+        err = P->mt == 1 ? launch_decode_t<64, 1, 2>(P, dp, stream) : launch_decode_t<64, 2, 2>(P, dp, stream);
+    else
+        err = P->mt == 1 ? launch_decode_t<128, 1, 2>(P, dp, stream) : launch_decode_t<128, 2, 2>(P, dp, stream);
+    if (err) return err;
+    if (H[H_N_RECORDS] > 0 && !dp.fused_merge)
+        err = launch_merge(H[H_N_REQ], c.num_q_heads, c.head_dim, P->d_meta + H[H_OFF_REC_PTR], P->d_part_o,
+                           P->d_part_lse, o, o_sr, o_sh, lse, l_sr, l_sh, P->num_ctas, stream);
+    return err;
+}
+
+}  // namespace spa

@@ -57,6 +57,7 @@ spa_status spa_plan_create(spa_pool* pool, const spa_plan_config* cfg, spa_plan*
     if (c.max_rows == 0) c.max_rows = 16;
     if (c.max_rows != 16 && c.max_rows != 32) return fail(SPA_ERR_UNSUPPORTED, "max_rows must be 16 or 32");
     if (c.split_pages < 0 || c.num_ctas < 0) return fail(SPA_ERR_INVALID_ARG, "negative plan option");
+    if (c.fused_merge < 0 || c.fused_merge > 2) return fail(SPA_ERR_INVALID_ARG, "fused_merge must be 0, 1 or 2");
     const int G = pool->cfg.num_q_heads / pool->cfg.num_kv_heads;
     if (G > c.max_rows) return fail(SPA_ERR_UNSUPPORTED, "GQA group size exceeds max_rows");
     spa_plan* P = new spa_plan();
@@ -66,7 +67,7 @@ spa_status spa_plan_create(spa_pool* pool, const spa_plan_config* cfg, spa_plan*
     int ctas = c.num_ctas;
     if (ctas == 0) ctas = pool->sm_count > 0 ? pool->sm_count : 148;
     P->num_ctas = ctas;
-    P->n_teams = ctas * (kWarps / P->mt);
+    P->n_teams = ctas * decode_teams_per_cta(P->mt);
     *out = P;
     return SPA_OK;
 }
@@ -185,6 +186,11 @@ spa_status spa_decode_plan(spa_plan* P, int32_t n_req, const spa_req* reqs, int3
             d.member_off = int32_t(members.size());
             d.n_members = int32_t(r.members.size());
             d.kind = r.kind;
+            // bit 2: the descriptor holds some member's newest token -- in a model step that
+            // key/value is produced right before attention, so the kernel does not prefetch
+            // it ahead of its programmatic-dependency wait
+            for (int m : r.members)
+                if (d.tok_end >= R[m]->len) d.kind |= 4;
             d.group = r.group;
             for (int32_t p = s; p < e; ++p) pages.push_back((*r.table)[p]);
             for (int m : r.members) {
@@ -217,7 +223,26 @@ spa_status spa_decode_plan(spa_plan* P, int32_t n_req, const spa_req* reqs, int3
     // atomic each, so faster SMs take more work and the tail is made of the smallest items
     std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return cost(x) > cost(y); });
     const int T = P->n_teams;
-    const int32_t sched[4] = {0, 0, 0, 0};   // [0] next queue slot, [1] teams finished (self-resetting)
+    // per layer: [0] next queue slot, [1] teams finished, [2] next tail-merge task (all
+    // self-resetting).  Per layer, so a layer's kernel may start popping while the previous
+    // layer's kernel drains (programmatic dependent launch).
+    const std::vector<int32_t> sched(size_t(pool->cfg.num_layers) * 4, 0);
+
+    // tail-merge tasks (fused_merge == 2): every (request with > 1 record, KV head), ordered
+    // by the queue position of its last item, so the earliest-complete merges come first
+    std::vector<int32_t> mtask;
+    {
+        std::vector<int32_t> last(size_t(n_req) * Hkv, -1);
+        for (int32_t qi = 0; qi < n_items; ++qi) {
+            const Item& itm = items[order[qi]];
+            const Desc& d = descs[itm.desc];
+            for (int32_t mi = d.member_off; mi < d.member_off + d.n_members; ++mi)
+                if (members[mi].rec >= 0) last[size_t(members[mi].row) * Hkv + itm.kv_head] = qi;
+        }
+        for (int32_t t = 0; t < int32_t(last.size()); ++t)
+            if (last[t] >= 0) mtask.push_back(t);
+        std::stable_sort(mtask.begin(), mtask.end(), [&](int32_t a, int32_t b) { return last[a] < last[b]; });
+    }
 
     // ---- 6. serialise: header + arrays (int32 words)
     std::vector<int32_t>& H = P->host;
@@ -231,7 +256,7 @@ spa_status spa_decode_plan(spa_plan* P, int32_t n_req, const spa_req* reqs, int3
     put(H_OFF_DESC, descs.data(), descs.size() * 8);
     put(H_OFF_MEMBER, members.data(), members.size() * 4);
     put(H_OFF_ITEM, items.data(), items.size() * 2);
-    put(H_OFF_SCHED, sched, 4);
+    put(H_OFF_SCHED, sched.data(), sched.size());
     put(H_OFF_QUEUE, order.data(), order.size());
     put(H_OFF_PAGES, pages.data(), pages.size());
     put(H_OFF_REC_PTR, rec_ptr.data(), rec_ptr.size());
@@ -239,6 +264,8 @@ spa_status spa_decode_plan(spa_plan* P, int32_t n_req, const spa_req* reqs, int3
         const std::vector<int32_t> zeros(size_t(n_req) * Hkv, 0);
         put(H_OFF_COUNTERS, zeros.data(), zeros.size());
     }
+    put(H_OFF_MTASK, mtask.data(), mtask.size());
+    H[H_N_MTASK] = int32_t(mtask.size());
     H[H_N_REQ] = n_req;
     H[H_N_DESC] = n_desc;
     H[H_N_ITEMS] = n_items;

@@ -27,7 +27,7 @@ enum MetaHeader : int {
     H_OFF_DESC = 5,
     H_OFF_MEMBER = 6,
     H_OFF_ITEM = 7,
-    H_OFF_SCHED = 8,       // int32[4]: dynamic queue head, finished-team count (both reset in-kernel)
+    H_OFF_SCHED = 8,       // int32[L][4]: per layer queue head, finished teams, tail-merge head (reset in-kernel)
     H_OFF_QUEUE = 9,       // int32[n_items]: item indices, largest first
     H_OFF_PAGES = 10,
     H_OFF_REC_PTR = 11,
@@ -35,7 +35,9 @@ enum MetaHeader : int {
     H_N_MEMBERS = 13,
     H_N_PAGES = 14,
     H_OFF_COUNTERS = 15,   // int32 [n_req][Hkv] arrival counters of the fused merge (zero between launches)
-    H_WORDS = 16
+    H_OFF_MTASK = 16,      // int32 [n_mtask]: (row * Hkv + kv_head) merge tasks, earliest-ready first
+    H_N_MTASK = 17,
+    H_WORDS = 20
 };
 
 // Work descriptor: keys [tok_start, tok_end) of one group-split or member-tail-split,
@@ -128,10 +130,9 @@ int launch_decode(const spa_plan* plan, int32_t layer, const void* q, int64_t q_
 int launch_merge(int32_t n_req, int32_t num_heads, int32_t head_dim, const int32_t* rec_ptr, const float* part_o,
                  const float* part_lse, void* o, int64_t o_sr, int64_t o_sh, float* lse, int64_t l_sr, int64_t l_sh,
                  int grid_hint, void* stream);
+int decode_teams_per_cta(int mt);   // decode.cu: work-item streams per CTA
 int memset_pool(spa_pool* pool);
 bool make_tensor_maps(spa_pool* pool, std::string* err);
 int device_sm_count(int* device_out);
 const char* cuda_error_string(int err);
-int stages_per_team(int head_dim, int mt);
-size_t decode_smem_bytes(int head_dim, int mt);
 }  // namespace spa

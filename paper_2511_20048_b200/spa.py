@@ -74,7 +74,46 @@ _SIGS = {
     "spa_abi_version": (c_int32, []),
     "spa_last_error": (ctypes.c_char_p, []),
     "spa_plan_debug_array": (c_int32, [c_void_p, c_int32, ctypes.POINTER(P_int32), P_int64, P_int32]),
+    "spa_debug_read_bw_ldg": (c_int32, [c_void_p, ctypes.c_size_t, c_void_p, c_void_p]),
+    "spa_debug_pool_read_tma": (c_int32, [c_void_p, c_int32, c_int32, c_void_p]),
 }
+
+
+def read_ceilings(pool: "Pool", scratch_bytes: int = 4 << 30, reps: int = 5, stream=None) -> dict:
+    """Same-run read-bandwidth ceilings (GB/s): streaming LDG over a scratch buffer, and the
+    decode kernel's TMA pipeline without math over the pool (include/spa_debug.h)."""
+    import torch  # noqa: WPS433
+
+    dev = pool.k.device
+    buf = torch.empty(scratch_bytes // 2, dtype=torch.bfloat16, device=dev)
+    buf.fill_(1.0)
+    sink = torch.zeros(4, dtype=torch.int32, device=dev)
+    s = _stream_ptr(stream)
+    out = {}
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    best = 0.0
+    for _ in range(reps):
+        ev[0].record()
+        _check(lib().spa_debug_read_bw_ldg(_ptr(buf), buf.numel() * 2, _ptr(sink), s))
+        ev[1].record()
+        torch.cuda.synchronize()
+        best = max(best, buf.numel() * 2 / (ev[0].elapsed_time(ev[1]) * 1e-3) / 1e9)
+    out["ldg_read_gbs"] = best
+    del buf
+    c = pool.cfg
+    per_layer = (c.num_pages // 2 * 2) * c.num_kv_heads * c.page_size * c.head_dim * 2 * 2
+    layers = max(1, min(c.num_layers, (8 << 30) // max(1, per_layer)))
+    for mode, name in ((0, "tma_pool_read_gbs"), (1, "tma3d_pool_read_gbs"), (2, "bulk_pool_read_gbs")):
+        best = 0.0
+        for _ in range(reps):
+            ev[0].record()
+            _check(lib().spa_debug_pool_read_tma(pool.h, layers, mode, s))
+            ev[1].record()
+            torch.cuda.synchronize()
+            best = max(best, layers * per_layer / (ev[0].elapsed_time(ev[1]) * 1e-3) / 1e9)
+        out[name] = best
+    out["tma_probe_bytes"] = layers * per_layer
+    return out
 
 _lib = None
 
@@ -246,9 +285,10 @@ class Pool:
 
 
 class Plan:
-    def __init__(self, pool: Pool, sharing=True, max_rows=16, split_pages=0, num_ctas=0, fused_merge=False):
+    def __init__(self, pool: Pool, sharing=True, max_rows=16, split_pages=0, num_ctas=0, fused_merge=0):
+        """fused_merge: 0 separate PDL merge kernel, 1 last-arriver in-kernel, 2 tail phase."""
         self.pool = pool
-        cfg = spa_plan_config(1 if sharing else 0, max_rows, split_pages, num_ctas, 1 if fused_merge else 0)
+        cfg = spa_plan_config(1 if sharing else 0, max_rows, split_pages, num_ctas, int(fused_merge))
         h = c_void_p()
         _check(lib().spa_plan_create(pool.h, ctypes.byref(cfg), ctypes.byref(h)))
         self.h = h

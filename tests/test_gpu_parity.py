@@ -9,6 +9,7 @@ import numpy as np
 import pytest
 import torch
 
+from gpu_compare import assert_bf16_close
 from harness import LSE_TOL, O_TOL, GpuBatch, bits_to_torch, compare, run_parity, torch_to_bits
 from oracle.attention import merge_partials
 from oracle.kvmodel import PagingModel
@@ -38,7 +39,9 @@ def test_tiny_config(prefix, family):
     """BJ config 0: 1 layer, 8 Q / 2 KV heads, d=64, reasoning request + 1 fork."""
     errs, outs, gb, plan, _ = run_parity(workloads.tiny(prefix), family)
     _assert_ok(errs)
-    assert errs[0][0] < 8e-3        # expected budget ~4e-3 (DESIGN.md Sec. 5)
+    # budget (DESIGN.md Sec. 5): bf16 P rounding <= 2^-9 max|v| + bf16 output rounding
+    # <= half an ulp of |O| < 4: 7.7e-3 + 7.8e-3
+    assert errs[0][0] < 1.6e-2
 
 
 @pytest.mark.parametrize("seed", range(10))
@@ -109,19 +112,19 @@ def test_split_merge_equals_unsplit():
     rec = workloads.random_small(11, workloads.Model("m", 1, 8, 2, 128), max_prefix=400)
     e1, out1, *_ = run_parity(rec, "peaky", split_pages=1000)
     e2, out2, *_ = run_parity(rec, "peaky", split_pages=1)
-    e3, out3, *_ = run_parity(rec, "peaky", split_pages=1, fused_merge=True)
-    _assert_ok(e1)
-    _assert_ok(e2)
-    _assert_ok(e3)
-    (o1, l1), (o2, l2), (o3, l3) = out1[0], out2[0], out3[0]
-    assert (o1.float() - o2.float()).abs().max().item() <= 8e-3
+    e3, out3, *_ = run_parity(rec, "peaky", split_pages=1, fused_merge=1)
+    e4, out4, *_ = run_parity(rec, "peaky", split_pages=1, fused_merge=2)
+    for e in (e1, e2, e3, e4):
+        _assert_ok(e)
+    (o1, l1), (o2, l2), (o3, l3), (o4, l4) = out1[0], out2[0], out3[0], out4[0]
+    assert_bf16_close(o1, o2)
     assert (l1 - l2).abs().max().item() <= 1e-4
-    # the fused in-kernel merge and the standalone merge kernel compute the same sums
-    assert (o2.float() - o3.float()).abs().max().item() <= 4e-3
-    assert (l2 - l3).abs().max().item() <= 1e-5
+    # the in-kernel merges and the standalone merge kernel run the same warp merge code
+    assert torch.equal(o2, o3) and torch.equal(l2, l3)
+    assert torch.equal(o2, o4) and torch.equal(l2, l4)
 
 
-@pytest.mark.parametrize("fused", [False, True])
+@pytest.mark.parametrize("fused", [0, 1, 2])
 @pytest.mark.parametrize("max_rows", [16, 32])
 def test_merge_paths_many_splits(fused, max_rows):
     """Many splits per request, both merge paths, two layers (counters reset between launches)."""
@@ -149,7 +152,7 @@ def test_sharing_on_off_agree():
     e2, b, *_ = run_parity(rec, "needle_shared_pos", sharing=False)
     _assert_ok(e1)
     _assert_ok(e2)
-    assert (a[0][0].float() - b[0][0].float()).abs().max().item() <= 8e-3
+    assert_bf16_close(a[0][0], b[0][0])
 
 
 def test_single_key_and_duplicated_heads():
