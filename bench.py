@@ -49,8 +49,8 @@ def parse():
                     help="cudaProfilerStart/Stop around the timed steps only (ncu --profile-from-start off); "
                          "skips parity, e2e and the cpu baseline")
     ap.add_argument("--sharing", type=int, default=1)
-    ap.add_argument("--fused-merge", type=int, default=0,
-                    help="0: PDL-chained merge kernel, 1: last-arriver in-kernel merge, 2: in-kernel tail phase")
+    ap.add_argument("--merge-mode", type=int, default=0,
+                    help="split merge: 0 in-kernel tail phase, 1 in-kernel last arriver, 2 PDL-chained merge kernel")
     ap.add_argument("--split-pages", type=int, default=0, help="max pages per split (0 = auto)")
     ap.add_argument("--layers", type=int, default=0, help="override resident layer count (0 = model's)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the oracle cpu_baseline sample")
@@ -271,7 +271,7 @@ def run_spa(args):
         o_all = torch.empty((L, N, hq_l, d), dtype=torch.bfloat16, device=dev)
         lse_all = torch.empty((L, N, hq_l), dtype=torch.float32, device=dev)
     plan = spa.Plan(pool, sharing=bool(args.sharing), split_pages=args.split_pages,
-                    fused_merge=args.fused_merge)
+                    merge_mode=args.merge_mode)
 
     state = {"step": 0}
 
@@ -351,12 +351,30 @@ def run_spa(args):
         ms = float(t.item())
     st = plan.stats()
 
-    # ---- per-launch decode timing (events around each spa_decode_attention call)
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * L)]
+    # ---- per-launch decode timing.  (a) chained: events around the whole layer loop of one
+    #      step (the launches stay PDL-chained exactly as in the timed steps), averaged per
+    #      layer; (b) isolated: events around each spa_decode_attention call.
+    def layer_loop():
+        for li in range(L):
+            if comm is None:
+                plan.decode(li, q_all[li], o_all[li], lse_all[li], scale=m.softmax_scale, stream=stream)
+            else:
+                plan.decode_sharded(comm, li, q_all[li], o_all[li], lse_all[li], scale=m.softmax_scale, stream=stream)
+
     barrier()
     pool.append(reqs, [1] * N, step_k[0], step_v[0], stream=stream)
     plan.plan(reqs, 0, stream=stream)
     st = plan.stats()
+    chained = []
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        layer_loop()
+        e1.record(stream)
+        barrier()
+        chained.append(e0.elapsed_time(e1) / L)
+    layer_ms = float(np.median(chained))
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * L)]
     for li in range(L):
         evs[2 * li].record(stream)
         if comm is None:
@@ -366,7 +384,7 @@ def run_spa(args):
         evs[2 * li + 1].record(stream)
     barrier()
     per_layer_ms = [evs[2 * i].elapsed_time(evs[2 * i + 1]) for i in range(L)]
-    layer_ms = float(np.mean(per_layer_ms[1:] if L > 1 else per_layer_ms))
+    layer_ms_isolated = float(np.mean(per_layer_ms[1:] if L > 1 else per_layer_ms))
 
     # algorithmic bytes of one decode_attention launch (per GPU): unique KV tokens read per
     # KV head x Hkv_l x d x 2 (K,V) x 2 B + Q + O (bf16) + LSE (fp32) + partials (fp32 w+r)
@@ -417,7 +435,7 @@ def run_spa(args):
     if rank == 0:
         cpu = cpu_baseline(recipe, batch, args.cpu_seconds) if world == 1 and not args.profile else None
         ck = clocks.summary(local)
-        sep = args.fused_merge == 0 and st["n_records"] > 0
+        sep = args.merge_mode == 2 and st["n_records"] > 0
         launches_per_step = (-(-N // 896)) + L * (2 if sep else 1)
         result = {
             "metric": METRIC,
@@ -440,11 +458,13 @@ def run_spa(args):
                        "l2": "inputs larger than L2 (KV per layer > 126 MB), no flush"},
             "gpu_launches": int(launches_per_step * args.steps),
             "layer_ms": layer_ms,
+            "layer_ms_isolated": layer_ms_isolated,
             "hbm_gbs_algorithmic": achieved,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"], "traffic": None,
                          "kernel": ("decode_kernel + merge_kernel (one spa_decode_attention call)" if sep
-                                    else "decode_kernel (split merge fused in-kernel)"),
+                                    else "decode_kernel (split merge in-kernel, tail phase)" if args.merge_mode == 0
+                                    else "decode_kernel (split merge in-kernel, last arriver)"),
                          "peak_kind": pk_kind, "alg_bytes_per_launch": int(alg_bytes),
                          "frac_of_8tbs": achieved / 8000.0,
                          "same_run_read_ceilings_gbs": ceilings,

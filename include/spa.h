@@ -128,11 +128,12 @@ typedef struct spa_plan_config {
                                are cut into sub-groups.  0 = 16                                 */
     int32_t split_pages;    /* max pages per split; 0 = auto (balance over the persistent grid)  */
     int32_t num_ctas;       /* persistent grid size; 0 = number of SMs                            */
-    int32_t fused_merge;    /* 0 (default): split partials are merged by a merge_kernel launched
-                               right after the decode kernel (programmatic dependent launch);
-                               1: inside the decode kernel by the last item of each (request, KV
-                               head); 2: inside the decode kernel, by teams that found the work
-                               queue empty (tail phase).  spa_merge_splits semantics always.     */
+    int32_t merge_mode;     /* where split partials are merged (spa_merge_splits semantics always):
+                               0 (default): inside the decode kernel, by teams that found the work
+                                 queue empty (tail phase);
+                               1: inside the decode kernel, by the last item of each (request, KV
+                                 head) to finish;
+                               2: by a separate merge_kernel launch (programmatic dependent launch) */
 } spa_plan_config;
 
 /* cfg may be NULL (defaults).  The plan keeps a pointer to `pool`. */

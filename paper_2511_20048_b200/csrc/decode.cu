@@ -545,7 +545,8 @@ __global__ void __launch_bounds__(kDecodeWarps * 32, 1)
             const int s0 = rec_ptr[row], s1 = rec_ptr[row + 1];
             if (producer && lane == 0) {
                 int* c = counters + task;
-                while (ld_acquire_gpu(c) < s1 - s0) __nanosleep(64);
+                // exponential backoff keeps hundreds of waiting teams off the L2 atomics
+                for (unsigned ns = 128; ld_acquire_gpu(c) < s1 - s0; ns = min(ns * 2, 2048u)) __nanosleep(ns);
                 *c = 0;   // all arrivals of this launch are in
             }
             team_sync();
@@ -605,7 +606,7 @@ int launch_decode(const spa_plan* P, int32_t layer, const void* q, int64_t q_sr,
     dp.num_q_heads = c.num_q_heads;
     dp.num_kv_heads = c.num_kv_heads;
     dp.group_size = c.num_q_heads / c.num_kv_heads;
-    dp.fused_merge = P->cfg.fused_merge;
+    dp.fused_merge = P->cfg.merge_mode == 0 ? 2 : P->cfg.merge_mode == 1 ? 1 : 0;
     dp.layer = layer;
     int err = 0;
     if (c.head_dim == 64)

@@ -57,7 +57,7 @@ spa_status spa_plan_create(spa_pool* pool, const spa_plan_config* cfg, spa_plan*
     if (c.max_rows == 0) c.max_rows = 16;
     if (c.max_rows != 16 && c.max_rows != 32) return fail(SPA_ERR_UNSUPPORTED, "max_rows must be 16 or 32");
     if (c.split_pages < 0 || c.num_ctas < 0) return fail(SPA_ERR_INVALID_ARG, "negative plan option");
-    if (c.fused_merge < 0 || c.fused_merge > 2) return fail(SPA_ERR_INVALID_ARG, "fused_merge must be 0, 1 or 2");
+    if (c.merge_mode < 0 || c.merge_mode > 2) return fail(SPA_ERR_INVALID_ARG, "merge_mode must be 0, 1 or 2");
     const int G = pool->cfg.num_q_heads / pool->cfg.num_kv_heads;
     if (G > c.max_rows) return fail(SPA_ERR_UNSUPPORTED, "GQA group size exceeds max_rows");
     spa_plan* P = new spa_plan();
@@ -228,7 +228,7 @@ spa_status spa_decode_plan(spa_plan* P, int32_t n_req, const spa_req* reqs, int3
     // layer's kernel drains (programmatic dependent launch).
     const std::vector<int32_t> sched(size_t(pool->cfg.num_layers) * 4, 0);
 
-    // tail-merge tasks (fused_merge == 2): every (request with > 1 record, KV head), ordered
+    // tail-merge tasks (merge_mode 0): every (request with > 1 record, KV head), ordered
     // by the queue position of its last item, so the earliest-complete merges come first
     std::vector<int32_t> mtask;
     {

@@ -84,11 +84,11 @@ def compare(o: torch.Tensor, lse: torch.Tensor, O_ref: np.ndarray, L_ref: np.nda
 
 
 def run_parity(recipe, family="flat", window=0, sharing=True, max_rows=16, split_pages=0, num_ctas=0,
-               layers=None, pre_shuffle=0, fused_merge=0):
+               layers=None, pre_shuffle=0, merge_mode=0):
     inp = families.make_inputs(recipe, family, layers=layers)
     gb = GpuBatch(inp, pre_shuffle=pre_shuffle)
     plan = spa.Plan(gb.pool, sharing=sharing, max_rows=max_rows, split_pages=split_pages, num_ctas=num_ctas,
-                    fused_merge=fused_merge)
+                    merge_mode=merge_mode)
     plan.plan(gb.reqs, window)
     rp = Replay(inp)
     errs = []

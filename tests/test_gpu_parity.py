@@ -111,9 +111,9 @@ def test_fork_equals_physical_copy():
 def test_split_merge_equals_unsplit():
     rec = workloads.random_small(11, workloads.Model("m", 1, 8, 2, 128), max_prefix=400)
     e1, out1, *_ = run_parity(rec, "peaky", split_pages=1000)
-    e2, out2, *_ = run_parity(rec, "peaky", split_pages=1)
-    e3, out3, *_ = run_parity(rec, "peaky", split_pages=1, fused_merge=1)
-    e4, out4, *_ = run_parity(rec, "peaky", split_pages=1, fused_merge=2)
+    e2, out2, *_ = run_parity(rec, "peaky", split_pages=1, merge_mode=2)
+    e3, out3, *_ = run_parity(rec, "peaky", split_pages=1, merge_mode=1)
+    e4, out4, *_ = run_parity(rec, "peaky", split_pages=1, merge_mode=0)
     for e in (e1, e2, e3, e4):
         _assert_ok(e)
     (o1, l1), (o2, l2), (o3, l3), (o4, l4) = out1[0], out2[0], out3[0], out4[0]
@@ -124,12 +124,12 @@ def test_split_merge_equals_unsplit():
     assert torch.equal(o2, o4) and torch.equal(l2, l4)
 
 
-@pytest.mark.parametrize("fused", [0, 1, 2])
+@pytest.mark.parametrize("mode", [0, 1, 2])
 @pytest.mark.parametrize("max_rows", [16, 32])
-def test_merge_paths_many_splits(fused, max_rows):
+def test_merge_paths_many_splits(mode, max_rows):
     """Many splits per request, both merge paths, two layers (counters reset between launches)."""
     rec = workloads.random_small(31, workloads.Model("m", 3, 16, 4, 128), max_prefix=500)
-    errs, *_ = run_parity(rec, "needle_shared_pos", split_pages=2, max_rows=max_rows, fused_merge=fused,
+    errs, *_ = run_parity(rec, "needle_shared_pos", split_pages=2, max_rows=max_rows, merge_mode=mode,
                           num_ctas=9)
     _assert_ok(errs)
 
