@@ -395,6 +395,15 @@ def run_spa(args):
     pk, pk_kind = peaks()
     achieved = alg_bytes / (layer_ms * 1e-3) / 1e9
     ceilings = spa.read_ceilings(pool) if not args.profile else None
+    # DRAM traffic per launch of the dominant kernel, from the committed ncu --set full capture
+    # of this configuration (profiles/latest_ncu.json); null if none matches
+    traffic = None
+    try:
+        nc = json.load(open(os.path.join(ROOT, "profiles", "latest_ncu.json")))
+        if nc.get("config") == args.config and world == 1 and args.sharing:
+            traffic = nc["traffic_bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        pass
 
     # ---- end-to-end through the public API with host buffers (pinned), copies inside
     e2e = None
@@ -461,7 +470,8 @@ def run_spa(args):
             "layer_ms_isolated": layer_ms_isolated,
             "hbm_gbs_algorithmic": achieved,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                         "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                         "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
+                         "traffic_source": "profiles/latest_ncu.json (ncu dram__bytes_read+write per launch)",
                          "kernel": ("decode_kernel + merge_kernel (one spa_decode_attention call)" if sep
                                     else "decode_kernel (split merge in-kernel, tail phase)" if args.merge_mode == 0
                                     else "decode_kernel (split merge in-kernel, last arriver)"),
