@@ -271,3 +271,43 @@ def test_append_decode_steps_and_free():
     rp.paging.free(rp.rid[victim])
     assert gb.pool.free_pages() == rp.paging.free_pages
     assert gb.pool.refcounts() == rp.paging.refcount
+    # ... and a new speculative request forks the same parent at its current length
+    parent = (victim[0], "main")
+    pst, ppages, plen = gb.pool.page_table(gb.ids[parent])
+    child = gb.pool.fork(gb.ids[parent], plen)
+    mst, mchild = rp.paging.fork(rp.rid[parent], plen)
+    assert (mst, mchild) == (0, child)
+    rp.kv.fork(("new", 0), parent, plen)
+    kb = kv_bits_np(98, KIND_K, 0, [0], np.arange(5), 2, 128)
+    vb = kv_bits_np(98, KIND_V, 0, [0], np.arange(5), 2, 128)
+    gb.pool.append([child], [5], bits_to_torch(kb), bits_to_torch(vb))
+    rp.kv.append(("new", 0), kb, vb)
+    rp.paging.append([mchild], [5])
+    names = [nm for nm in inp.batch if nm != victim] + [("new", 0)]
+    reqs = [gb.ids[nm] for nm in inp.batch if nm != victim] + [child]
+    plan.plan(reqs)
+    qb = families.kv_bits_np(5, 3, 90, [0], np.arange(len(reqs)), 8, 128)[0]
+    o, lse = plan.decode(0, bits_to_torch(qb), scale=rec.model.softmax_scale)
+    torch.cuda.synchronize()
+    O, L = rp.expected(0, qb, names=names)
+    eo, el = compare(o, lse, O, L)
+    assert eo <= O_TOL and el <= LSE_TOL
+    assert gb.pool.page_table(child)[1:] == rp.paging.page_table(mchild)[1:]
+
+
+def test_sharded_single_rank_layout():
+    """spa_decode_attention_sharded with a 1-rank comm writes the head-major gather layout
+    [Hq][N][d] (+ LSE [Hq][N]) bit-identically to spa_decode_attention."""
+    rec = workloads.random_small(13, workloads.Model("m", 1, 10, 2, 128), max_prefix=200)
+    errs, outs, gb, plan, rp = run_parity(rec, "flat", split_pages=3)
+    _assert_ok(errs)
+    o_ref, l_ref = outs[0]
+    N, Hq, d = o_ref.shape
+    comm = spa.Comm(b"\0" * 128, 0, 1)
+    og = torch.empty((Hq, N, d), dtype=torch.bfloat16, device="cuda")
+    lg = torch.empty((Hq, N), dtype=torch.float32, device="cuda")
+    q = bits_to_torch(gb.inputs.q[0]).contiguous()
+    plan.decode_sharded(comm, 0, q, og, lg, scale=rec.model.softmax_scale)
+    torch.cuda.synchronize()
+    assert torch.equal(og.permute(1, 0, 2), o_ref) and torch.equal(lg.t(), l_ref)
+    comm.close()
