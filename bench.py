@@ -1,20 +1,25 @@
 """Benchmark of the SPAgent decode-attention step (BASELINE.json metric) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config qwen|tiny|gemma|long]
-                    [--impl spa|reference] [--no-parity] [--no-e2e]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config qwen|gemma|long|tiny]
+                    [--impl spa|reference] [--no-parity] [--no-e2e] [--graph]
 
 A step = one pass of the whole hot path over one batch:
   a2 spa_kv_append of one new token per request (all layers),
-  a4 spa_decode_plan (host planning + one upload),
-  a5+a6 spa_decode_attention for every layer (decode kernel + split merge),
+  a4 spa_decode_plan (host planning + one upload; one plan per distinct window),
+  a5+a6 spa_decode_attention for every layer of the model (decode kernel; split merge
+        in-kernel by default),
   a7 (N > 1) the NCCL all-gather of head-sharded outputs.
-Fork/alloc/free (a1, a3, a8) build the batch before timing (host calls; the
-copy-on-write kernels run there).
+Fork/alloc/free (a1, a3, a8) build the batch before timing (host calls; the copy-on-write
+kernels run there).
 
-Default workload: BJ config 1 (Qwen2.5-32B attention: 40 Q / 8 KV heads, d=128, 64
-layers, 32 agents + 32 speculative forks, contexts 2k-8k), synthetic seeded data.
-value = decode tokens/s = N_requests / step time (each request decodes one token per
-step through all 64 layers), max over ranks.  Prints ONE JSON line on rank 0.
+Default workload: BJ config 1 (Qwen2.5-32B attention: 40 Q / 8 KV heads, d=128, 64 layers,
+32 agents + 32 speculative forks, contexts 2k-8k), synthetic seeded data, all 64 layers
+resident.  value = decode tokens/s = N_requests / step time (each request decodes one
+token per step through all layers), max over ranks.  Prints ONE JSON line on rank 0.
+
+--config gemma (BJ config 2): 62 attention calls per step, 52 with a 1024-token sliding
+window (5:1 local/global), over 6 resident layers (call i reads resident layer i % 6; each
+layer's KV is far larger than L2, so reuse gives no cache benefit).
 """
 from __future__ import annotations
 
@@ -33,10 +38,19 @@ sys.path.insert(0, ROOT)
 from spa_inputs import KIND_K, KIND_Q, KIND_V, kv_bits_np, kv_bits_torch, workloads  # noqa: E402
 from spa_inputs.families import origin_id  # noqa: E402
 
+_T0 = time.time()
+
+
+def _log(*a):
+    """Progress on stderr (the JSON line on stdout stays the only stdout output)."""
+    print(f"[bench {time.time() - _T0:7.1f}s]", *a, file=sys.stderr, flush=True)
+
+
 METRIC = "decode-attn tokens/s and achieved HBM GB/s (% of peak) at 1/2/4/8 B200"
+BJ_INDEX = {"tiny": 0, "qwen": 1, "gemma": 2, "long": 4}
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -45,6 +59,7 @@ def parse():
     ap.add_argument("--impl", default="spa", choices=["spa", "reference"])
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--graph", action="store_true", help="replay the per-step layer loop as a CUDA graph")
     ap.add_argument("--profile", action="store_true",
                     help="cudaProfilerStart/Stop around the timed steps only (ncu --profile-from-start off); "
                          "skips parity, e2e and the cpu baseline")
@@ -52,9 +67,9 @@ def parse():
     ap.add_argument("--merge-mode", type=int, default=0,
                     help="split merge: 0 in-kernel tail phase, 1 in-kernel last arriver, 2 PDL-chained merge kernel")
     ap.add_argument("--split-pages", type=int, default=0, help="max pages per split (0 = auto)")
-    ap.add_argument("--layers", type=int, default=0, help="override resident layer count (0 = model's)")
+    ap.add_argument("--layers", type=int, default=0, help="resident layers (0 = config default)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the oracle cpu_baseline sample")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 def recipe_for(name):
@@ -62,11 +77,24 @@ def recipe_for(name):
             "long": workloads.long32k}[name]()
 
 
+def default_resident_layers(name, model):
+    return {"gemma": 6, "long": 4}.get(name, model.num_layers)
+
+
 def peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
     except (OSError, ValueError):
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def layer_schedule(recipe, resident):
+    """[(resident layer, window)] of the attention calls of one model step."""
+    m = recipe.model
+    if recipe.local_layers:
+        local = set(recipe.local_layers)
+        return [(i % resident, recipe.window if i in local else 0) for i in range(m.num_layers)]
+    return [(i, 0) for i in range(resident)]
 
 
 # ----------------------------------------------------------------------------- oracle (cpu)
@@ -86,13 +114,8 @@ def logical_kv_np(recipe, gi, who, layers, kind):
     return np.concatenate([a, b], axis=1)
 
 
-def step_token_bits(recipe, layers, n_req, step_origin, kind):
-    m = recipe.model
-    return kv_bits_np(recipe.seed, kind, step_origin, layers, np.arange(n_req), m.num_kv_heads, m.head_dim)
-
-
-def oracle_sample(recipe, batch, rows, layer_pos, layers, q_bits, steps_appended):
-    """fp64 oracle outputs for batch rows `rows` at one layer (O [r, Hq, d], LSE [r, Hq])."""
+def oracle_sample(recipe, batch, rows, layer, q_bits, steps_appended, window=0):
+    """fp64 oracle outputs for batch rows `rows` at one (resident) layer."""
     from oracle.attention import decode_attention
     from oracle.replay import bits_to_f64
 
@@ -100,12 +123,14 @@ def oracle_sample(recipe, batch, rows, layer_pos, layers, q_bits, steps_appended
     out_o, out_l = [], []
     for r in rows:
         gi, who = batch[r]
-        K = logical_kv_np(recipe, gi, who, [layers[layer_pos]], KIND_K)[0]
-        V = logical_kv_np(recipe, gi, who, [layers[layer_pos]], KIND_V)[0]
+        K = logical_kv_np(recipe, gi, who, [layer], KIND_K)[0]
+        V = logical_kv_np(recipe, gi, who, [layer], KIND_V)[0]
         for s in range(steps_appended):
-            K = np.concatenate([K, step_token_bits(recipe, [layers[layer_pos]], len(batch), 500_000 + s, KIND_K)[0, r:r + 1]])
-            V = np.concatenate([V, step_token_bits(recipe, [layers[layer_pos]], len(batch), 500_000 + s, KIND_V)[0, r:r + 1]])
-        O, L = decode_attention(bits_to_f64(q_bits[r]), bits_to_f64(K), bits_to_f64(V), m.softmax_scale, 0)
+            kb = kv_bits_np(recipe.seed, KIND_K, 500_000 + s, [layer], np.arange(len(batch)), m.num_kv_heads, m.head_dim)
+            vb = kv_bits_np(recipe.seed, KIND_V, 500_000 + s, [layer], np.arange(len(batch)), m.num_kv_heads, m.head_dim)
+            K = np.concatenate([K, kb[0, r:r + 1]])
+            V = np.concatenate([V, vb[0, r:r + 1]])
+        O, L = decode_attention(bits_to_f64(q_bits[r]), bits_to_f64(K), bits_to_f64(V), m.softmax_scale, window)
         out_o.append(O)
         out_l.append(L)
     return np.stack(out_o), np.stack(out_l)
@@ -114,30 +139,35 @@ def oracle_sample(recipe, batch, rows, layer_pos, layers, q_bits, steps_appended
 def cpu_baseline(recipe, batch, budget_s):
     """The oracle as it stands, timed on this host's cores on a bounded sample of the
     workload: whole requests at one layer until ~budget_s of CPU work, scaled to tokens/s
-    of the full model (one token = one request through all layers)."""
+    of the full model step (one token = one request through all of the step's layer calls,
+    each at its own window)."""
+    from oracle.attention import decode_attention
+    from oracle.replay import bits_to_f64
+
     m = recipe.model
+    sched = layer_schedule(recipe, default_resident_layers("gemma" if recipe.local_layers else "x", m))
+    windows = sorted({w for _, w in sched})
+    calls_per_window = {w: sum(1 for _, ww in sched if ww == w) for w in windows}
     rng = np.random.default_rng(0)
     order = rng.permutation(len(batch))
     q = kv_bits_np(recipe.seed, KIND_Q, 1_000_000, [0], np.arange(len(batch)), m.num_q_heads, m.head_dim)[0]
     done = 0
-    t_work = 0.0
+    t_work = {w: 0.0 for w in windows}
     t0 = time.perf_counter()
     for r in order:
-        from oracle.attention import decode_attention
-        from oracle.replay import bits_to_f64
-
         gi, who = batch[r]
         K = bits_to_f64(logical_kv_np(recipe, gi, who, [0], KIND_K)[0])
         V = bits_to_f64(logical_kv_np(recipe, gi, who, [0], KIND_V)[0])
         qf = bits_to_f64(q[r])
-        ts = time.perf_counter()
-        decode_attention(qf, K, V, m.softmax_scale, 0)
-        t_work += time.perf_counter() - ts
+        for w in windows:
+            ts = time.perf_counter()
+            decode_attention(qf, K, V, m.softmax_scale, w)
+            t_work[w] += time.perf_counter() - ts
         done += 1
         if time.perf_counter() - t0 > budget_s:
             break
-    per_req_layer = t_work / done
-    tok_s = 1.0 / (per_req_layer * m.num_layers)
+    per_req_step = sum(t_work[w] / done * calls_per_window[w] for w in windows)
+    tok_s = 1.0 / per_req_step
     cores = os.cpu_count()
     try:
         import threadpoolctl
@@ -147,8 +177,8 @@ def cpu_baseline(recipe, batch, budget_s):
     except Exception:  # noqa: BLE001
         pass
     return {"value": tok_s, "unit": "tokens/s", "cores": cores, "kind": "oracle",
-            "sample": f"{done} of {len(batch)} requests x 1 layer (fp64 NumPy, BLAS dgemm per KV head), "
-                      f"{per_req_layer * 1e3:.2f} ms per request-layer, scaled x{m.num_layers} layers"}
+            "sample": f"{done} of {len(batch)} requests x 1 layer per window {windows} (fp64 NumPy, BLAS dgemm "
+                      f"per KV head), {per_req_step * 1e3:.1f} ms per request-step over {len(sched)} layer calls"}
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -196,6 +226,65 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# ----------------------------------------------------------------------------- batch build
+def build_batch(spa, pool, recipe, layers, kv_sl, dev, fill="hash", chunk=256):
+    """Replay the recipe's call log through the C ABI (a1 alloc, a2 append, a3 fork).
+
+    fill="hash": every appended token carries its own counter-hash K/V (parity-checkable);
+    fill="reuse": one chunk of counter-hash values is appended repeatedly (throughput
+    sweeps: timing does not depend on the values).
+    """
+    import torch
+
+    m = recipe.model
+    ops, batch = workloads.call_log(recipe)
+    ids = {}
+    reuse = None
+    if fill == "reuse":
+        pos = np.arange(chunk)
+        reuse = (kv_bits_torch(recipe.seed, KIND_K, 0, layers, pos, m.num_kv_heads, m.head_dim, dev)[:, :, kv_sl]
+                 .contiguous(),
+                 kv_bits_torch(recipe.seed, KIND_V, 0, layers, pos, m.num_kv_heads, m.head_dim, dev)[:, :, kv_sl]
+                 .contiguous())
+    for op in ops:
+        if op[0] == "alloc":
+            ids[op[1]] = pool.alloc()
+        elif op[0] == "append":
+            _, name, origin, start, n = op
+            for s0 in range(start, start + n, chunk):
+                s1 = min(start + n, s0 + chunk)
+                if reuse is not None:
+                    k, v = reuse[0][:, :s1 - s0].contiguous(), reuse[1][:, :s1 - s0].contiguous()
+                else:
+                    pos = np.arange(s0, s1)
+                    k = kv_bits_torch(recipe.seed, KIND_K, origin_id(origin), layers, pos, m.num_kv_heads,
+                                      m.head_dim, dev)[:, :, kv_sl].contiguous()
+                    v = kv_bits_torch(recipe.seed, KIND_V, origin_id(origin), layers, pos, m.num_kv_heads,
+                                      m.head_dim, dev)[:, :, kv_sl].contiguous()
+                pool.append([ids[name]], [s1 - s0], k, v)
+        elif op[0] == "fork":
+            ids[op[1]] = pool.fork(ids[op[2]], op[3])
+    torch.cuda.synchronize()
+    return ids, [ids[nm] for nm in batch], batch
+
+
+def pages_for(recipe, extra_tokens):
+    pages = 8
+    for g in recipe.groups:
+        pages += -(-(g.prefix + (g.parent_tail or 0) + extra_tokens) // 16)
+        pages += sum(-(-(ft + 16 + extra_tokens) // 16) for ft in g.fork_tails)
+    return pages
+
+
+def alg_bytes(st, N, hkv_l, hq_l, d):
+    """Algorithmic bytes of one decode_attention launch (per GPU): unique KV tokens per KV
+    head x Hkv_l x d x 2 (K, V) x 2 B + Q + O (bf16) + LSE (fp32) + partials (fp32, w+r)."""
+    kv = st["unique_tokens"] * hkv_l * d * 2 * 2
+    qo = N * hq_l * d * 2 * 2 + N * hq_l * 4
+    part = st["n_records"] * hq_l * (d + 1) * 4 * 2
+    return kv + qo + part
+
+
 # ----------------------------------------------------------------------------- main arm
 def run_spa(args):
     import torch
@@ -215,47 +304,30 @@ def run_spa(args):
 
     recipe = recipe_for(args.config)
     m = recipe.model
-    L = args.layers or m.num_layers
-    layers = list(range(L))
-    assert m.num_kv_heads % world == 0
-    hkv_l, hq_l = m.num_kv_heads // world, m.num_q_heads // world
-    kv_sl = slice(rank * hkv_l, (rank + 1) * hkv_l)
-    q_sl = slice(rank * hq_l, (rank + 1) * hq_l)
+    Lr = args.layers or default_resident_layers(args.config, m)
+    layers = list(range(Lr))
+    sched = layer_schedule(recipe, Lr)
+    C = len(sched)
+    windows = sorted({w for _, w in sched})
+    q_sl, kv_sl = spa.shard_heads(m.num_q_heads, m.num_kv_heads, rank, world)
+    hkv_l, hq_l = kv_sl.stop - kv_sl.start, q_sl.stop - q_sl.start
     d = m.head_dim
-    ops, batch = workloads.call_log(recipe)
-    N = len(batch)
-    total_steps = args.warmup + args.steps + 16
-    pages = 8
-    for g in recipe.groups:
-        pages += -(-(g.prefix + (g.parent_tail or 0) + total_steps) // 16)
-        pages += sum(-(-(ft + 16 + total_steps) // 16) for ft in g.fork_tails)
-    pool = spa.Pool(L, hq_l, hkv_l, d, pages, device=dev)
-    stream = torch.cuda.current_stream()
+    total_steps = args.warmup + args.steps + 32
+    # one non-default stream carries every launch and copy (CUDA-graph capture needs a
+    # non-legacy stream); torch ops use it as their current stream
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    pool = spa.Pool(Lr, hq_l, hkv_l, d, pages_for(recipe, total_steps), device=dev)
 
-    # ---- build the batch through the C ABI (a1 alloc, a2 append, a3 fork)
     t_build = time.perf_counter()
-    ids = {}
-    CH = 256
-    for op in ops:
-        if op[0] == "alloc":
-            ids[op[1]] = pool.alloc()
-        elif op[0] == "append":
-            _, name, origin, start, n = op
-            for s0 in range(start, start + n, CH):
-                s1 = min(start + n, s0 + CH)
-                pos = np.arange(s0, s1)
-                k = kv_bits_torch(recipe.seed, KIND_K, origin_id(origin), layers, pos, m.num_kv_heads, d, dev)
-                v = kv_bits_torch(recipe.seed, KIND_V, origin_id(origin), layers, pos, m.num_kv_heads, d, dev)
-                pool.append([ids[name]], [s1 - s0], k[:, :, kv_sl].contiguous(), v[:, :, kv_sl].contiguous())
-        elif op[0] == "fork":
-            ids[op[1]] = pool.fork(ids[op[2]], op[3])
-    reqs = [ids[nm] for nm in batch]
-    torch.cuda.synchronize()
+    ids, reqs, batch = build_batch(spa, pool, recipe, layers, kv_sl, dev)
     t_build = time.perf_counter() - t_build
+    _log('built batch', t_build)
+    N = len(batch)
 
     # ---- per-step inputs (resident in HBM for the device-timed value)
-    q_all = kv_bits_torch(recipe.seed, KIND_Q, 1_000_000, layers, np.arange(N), m.num_q_heads, d, dev)[:, :, q_sl]
-    q_all = q_all.contiguous()                                   # [L, N, Hq_l, d]
+    q_res = kv_bits_torch(recipe.seed, KIND_Q, 1_000_000, layers, np.arange(N), m.num_q_heads, d, dev)[:, :, q_sl]
+    q_all = torch.stack([q_res[r] for r, _ in sched]).contiguous()          # [C, N, Hq_l, d]
     step_k = [kv_bits_torch(recipe.seed, KIND_K, 500_000 + s, layers, np.arange(N), m.num_kv_heads, d, dev)[:, :, kv_sl]
               .contiguous() for s in range(2)]
     step_v = [kv_bits_torch(recipe.seed, KIND_V, 500_000 + s, layers, np.arange(N), m.num_kv_heads, d, dev)[:, :, kv_sl]
@@ -264,16 +336,22 @@ def run_spa(args):
         comm_id = [spa.spa_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(comm_id, src=0)
         comm = spa.Comm(comm_id[0], rank, world)
-        o_all = torch.empty((L, m.num_q_heads, N, d), dtype=torch.bfloat16, device=dev)   # gathered, head-major
-        lse_all = torch.empty((L, m.num_q_heads, N), dtype=torch.float32, device=dev)
+        o_all = torch.empty((C, m.num_q_heads, N, d), dtype=torch.bfloat16, device=dev)   # gathered, head-major
+        lse_all = torch.empty((C, m.num_q_heads, N), dtype=torch.float32, device=dev)
     else:
         comm = None
-        o_all = torch.empty((L, N, hq_l, d), dtype=torch.bfloat16, device=dev)
-        lse_all = torch.empty((L, N, hq_l), dtype=torch.float32, device=dev)
-    plan = spa.Plan(pool, sharing=bool(args.sharing), split_pages=args.split_pages,
-                    merge_mode=args.merge_mode)
+        o_all = torch.empty((C, N, hq_l, d), dtype=torch.bfloat16, device=dev)
+        lse_all = torch.empty((C, N, hq_l), dtype=torch.float32, device=dev)
+    plans = {w: spa.Plan(pool, sharing=bool(args.sharing), split_pages=args.split_pages, merge_mode=args.merge_mode)
+             for w in windows}
+    state = {"step": 0, "graph": None}
 
-    state = {"step": 0}
+    def layer_loop(qq, oo, ll):
+        for ci, (r, w) in enumerate(sched):
+            if comm is None:
+                plans[w].decode(r, qq[ci], oo[ci], ll[ci], scale=m.softmax_scale, stream=stream)
+            else:
+                plans[w].decode_sharded(comm, r, qq[ci], oo[ci], ll[ci], scale=m.softmax_scale, stream=stream)
 
     def one_step(kk, vv, qq=None, oo=None, ll=None):
         qq = q_all if qq is None else qq
@@ -282,12 +360,12 @@ def run_spa(args):
         s = state["step"]
         pool.append(reqs, [1] * N, kk[s % 2] if isinstance(kk, list) else kk,
                     vv[s % 2] if isinstance(vv, list) else vv, stream=stream)
-        plan.plan(reqs, 0, stream=stream)
-        for li in range(L):
-            if comm is None:
-                plan.decode(li, qq[li], oo[li], ll[li], scale=m.softmax_scale, stream=stream)
-            else:
-                plan.decode_sharded(comm, li, qq[li], oo[li], ll[li], scale=m.softmax_scale, stream=stream)
+        for w, p in plans.items():
+            p.plan(reqs, w, stream=stream)
+        if state["graph"] is not None and qq is q_all and oo is o_all:
+            state["graph"].replay()
+        else:
+            layer_loop(qq, oo, ll)
         state["step"] = s + 1
 
     def barrier():
@@ -295,39 +373,54 @@ def run_spa(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # ---- parity gate: the first step's sampled outputs vs the fp64 oracle (rank 0's heads
-    #      for N=1, the gathered heads for N>1), at layers 0 and L-1
+    # ---- parity gate: the first step's sampled outputs vs the fp64 oracle
     parity = None
     one_step(step_k, step_v)
     torch.cuda.synchronize()
     if args.profile:
         args.no_parity = args.no_e2e = True
     if not args.no_parity and rank == 0:
-        gsel = [0, len(recipe.groups) // 2]
+        gsel = sorted({0, len(recipe.groups) // 2})
         rows = [i for i, nm in enumerate(batch) if nm[0] in gsel]
+        calls = sorted({0, C - 1} | {next((i for i, (_, w) in enumerate(sched) if w == 0), 0)})
         worst_o = worst_l = 0.0
-        for lp in sorted({0, L - 1}):
-            qb = kv_bits_np(recipe.seed, KIND_Q, 1_000_000, [layers[lp]], np.arange(N), m.num_q_heads, d)[0]
-            O, Lr = oracle_sample(recipe, batch, rows, lp, layers, qb, steps_appended=1)
+        for ci in calls:
+            r, w = sched[ci]
+            qb = kv_bits_np(recipe.seed, KIND_Q, 1_000_000, [r], np.arange(N), m.num_q_heads, d)[0]
+            O, Lo = oracle_sample(recipe, batch, rows, r, qb, steps_appended=1, window=w)
             if comm is None:
-                og = o_all[lp, rows].float().cpu().numpy()
-                lg = lse_all[lp, rows].cpu().numpy()
-                O, Lr = O[:, q_sl], Lr[:, q_sl]
+                og = o_all[ci, rows].float().cpu().numpy()
+                lg = lse_all[ci, rows].cpu().numpy()
+                O, Lo = O[:, q_sl], Lo[:, q_sl]
             else:
-                og = o_all[lp][:, rows].permute(1, 0, 2).float().cpu().numpy()
-                lg = lse_all[lp][:, rows].permute(1, 0).cpu().numpy()
+                og = o_all[ci][:, rows].permute(1, 0, 2).float().cpu().numpy()
+                lg = lse_all[ci][:, rows].permute(1, 0).cpu().numpy()
             worst_o = max(worst_o, float(np.abs(og - O).max()))
-            worst_l = max(worst_l, float(np.abs(lg - Lr).max()))
-        parity = {"max_abs_o": worst_o, "max_abs_lse": worst_l, "rows": len(rows), "layers": sorted({0, L - 1}),
+            worst_l = max(worst_l, float(np.abs(lg - Lo).max()))
+        parity = {"max_abs_o": worst_o, "max_abs_lse": worst_l, "rows": len(rows),
+                  "calls": [{"call": ci, "layer": sched[ci][0], "window": sched[ci][1]} for ci in calls],
                   "pass": worst_o <= 2e-2 and worst_l <= 1e-3}
         if not parity["pass"]:
             print(json.dumps({"error": "parity gate failed", "parity": parity}))
             sys.exit(1)
 
+    _log('parity', parity)
+    # ---- optional CUDA graph of the layer loop (plan device buffers are stable across steps)
+    if args.graph:
+        gens = {w: p.stats()["generation"] for w, p in plans.items()}
+        g = torch.cuda.CUDAGraph()
+        barrier()
+        with torch.cuda.graph(g, stream=stream):
+            layer_loop(q_all, o_all, lse_all)
+        state["graph"] = g
+        barrier()
+
     # ---- warm-up, then K timed steps (device events on the launching stream)
     for _ in range(args.warmup):
         one_step(step_k, step_v)
     barrier()
+    if args.graph:
+        assert all(p.stats()["generation"] == gens[w] for w, p in plans.items()), "plan buffers moved"
     clocks = Clocks(os.path.join(ROOT, "gpurun_out", f"clocks_rank{rank}.csv")
                     if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else f"/tmp/spa_clocks_{rank}.csv")
     ev0 = torch.cuda.Event(enable_timing=True)
@@ -345,58 +438,61 @@ def run_spa(args):
         if args.profile:
             torch.cuda.profiler.stop()
     ms = ev0.elapsed_time(ev1) / args.steps
+    _log('timed steps', ms)
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    st = plan.stats()
 
-    # ---- per-launch decode timing.  (a) chained: events around the whole layer loop of one
-    #      step (the launches stay PDL-chained exactly as in the timed steps), averaged per
-    #      layer; (b) isolated: events around each spa_decode_attention call.
-    def layer_loop():
-        for li in range(L):
-            if comm is None:
-                plan.decode(li, q_all[li], o_all[li], lse_all[li], scale=m.softmax_scale, stream=stream)
-            else:
-                plan.decode_sharded(comm, li, q_all[li], o_all[li], lse_all[li], scale=m.softmax_scale, stream=stream)
-
+    # ---- per-launch timing per window class: events around the chained loop of every call
+    #      of that class (PDL chaining as in the step), and around each call in isolation
     barrier()
     pool.append(reqs, [1] * N, step_k[0], step_v[0], stream=stream)
-    plan.plan(reqs, 0, stream=stream)
-    st = plan.stats()
-    chained = []
-    for _ in range(3):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        layer_loop()
-        e1.record(stream)
-        barrier()
-        chained.append(e0.elapsed_time(e1) / L)
-    layer_ms = float(np.median(chained))
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * L)]
-    for li in range(L):
-        evs[2 * li].record(stream)
-        if comm is None:
-            plan.decode(li, q_all[li], o_all[li], lse_all[li], scale=m.softmax_scale, stream=stream)
-        else:
-            plan.decode_sharded(comm, li, q_all[li], o_all[li], lse_all[li], scale=m.softmax_scale, stream=stream)
-        evs[2 * li + 1].record(stream)
-    barrier()
-    per_layer_ms = [evs[2 * i].elapsed_time(evs[2 * i + 1]) for i in range(L)]
-    layer_ms_isolated = float(np.mean(per_layer_ms[1:] if L > 1 else per_layer_ms))
-
-    # algorithmic bytes of one decode_attention launch (per GPU): unique KV tokens read per
-    # KV head x Hkv_l x d x 2 (K,V) x 2 B + Q + O (bf16) + LSE (fp32) + partials (fp32 w+r)
-    kv_bytes = st["unique_tokens"] * hkv_l * d * 2 * 2
-    qo_bytes = N * hq_l * d * 2 * 2 + N * hq_l * 4
-    part_bytes = st["n_records"] * hq_l * (d + 1) * 4 * 2
-    alg_bytes = kv_bytes + qo_bytes + part_bytes
+    for w, p in plans.items():
+        p.plan(reqs, w, stream=stream)
+    per_window = {}
+    for w in windows:
+        cis = [ci for ci, (_, ww) in enumerate(sched) if ww == w]
+        chained = []
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for ci in cis:
+                r = sched[ci][0]
+                if comm is None:
+                    plans[w].decode(r, q_all[ci], o_all[ci], lse_all[ci], scale=m.softmax_scale, stream=stream)
+                else:
+                    plans[w].decode_sharded(comm, r, q_all[ci], o_all[ci], lse_all[ci], scale=m.softmax_scale,
+                                            stream=stream)
+            e1.record(stream)
+            barrier()
+            chained.append(e0.elapsed_time(e1) / len(cis))
+        iso = []
+        for ci in cis[: min(len(cis), 16)]:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r = sched[ci][0]
+            if comm is None:
+                plans[w].decode(r, q_all[ci], o_all[ci], lse_all[ci], scale=m.softmax_scale, stream=stream)
+            else:
+                plans[w].decode_sharded(comm, r, q_all[ci], o_all[ci], lse_all[ci], scale=m.softmax_scale,
+                                        stream=stream)
+            e1.record(stream)
+            barrier()
+            iso.append(e0.elapsed_time(e1))
+        st = plans[w].stats()
+        per_window[w] = {"calls": len(cis), "layer_ms": float(np.median(chained)),
+                         "layer_ms_isolated": float(np.median(iso)), "stats": st,
+                         "alg_bytes": alg_bytes(st, N, hkv_l, hq_l, d)}
+    _log('per-window timing done')
+    # the dominant launch class: most total time per step
+    wdom = max(windows, key=lambda w: per_window[w]["layer_ms"] * per_window[w]["calls"])
+    dom = per_window[wdom]
+    st = dom["stats"]
     pk, pk_kind = peaks()
-    achieved = alg_bytes / (layer_ms * 1e-3) / 1e9
+    achieved = dom["alg_bytes"] / (dom["layer_ms"] * 1e-3) / 1e9
     ceilings = spa.read_ceilings(pool) if not args.profile else None
-    # DRAM traffic per launch of the dominant kernel, from the committed ncu --set full capture
-    # of this configuration (profiles/latest_ncu.json); null if none matches
+    _log('ceilings', ceilings)
     traffic = None
     try:
         nc = json.load(open(os.path.join(ROOT, "profiles", "latest_ncu.json")))
@@ -444,8 +540,12 @@ def run_spa(args):
     if rank == 0:
         cpu = cpu_baseline(recipe, batch, args.cpu_seconds) if world == 1 and not args.profile else None
         ck = clocks.summary(local)
-        sep = args.merge_mode == 2 and st["n_records"] > 0
-        launches_per_step = (-(-N // 896)) + L * (2 if sep else 1)
+        sep = args.merge_mode == 2
+        launches_per_step = (-(-N // 896)) + sum(
+            1 + (1 if sep and per_window[w]["stats"]["n_records"] > 0 else 0) for _, w in sched)
+        kname = {0: "decode_kernel (split merge in-kernel, tail phase)",
+                 1: "decode_kernel (split merge in-kernel, last arriver)",
+                 2: "decode_kernel + merge_kernel (one spa_decode_attention call)"}[args.merge_mode]
         result = {
             "metric": METRIC,
             "value": N / (ms * 1e-3),
@@ -459,23 +559,26 @@ def run_spa(args):
             "vs_baseline": None,
             "dtype": "bf16",
             "data": "synthetic (seeded counter-hash bf16 K/V/Q, agent-shaped batch recipe)",
-            "config": {"workload": recipe.name + " (BJ config 1)" if args.config == "qwen" else recipe.name,
-                       "n_requests": N, "agents": len(recipe.groups), "layers": L,
+            "config": {"workload": f"{recipe.name} (BJ config {BJ_INDEX[args.config]})",
+                       "n_requests": N, "agents": len(recipe.groups), "layer_calls_per_step": C,
+                       "resident_layers": Lr, "windows": windows,
                        "q_heads": m.num_q_heads, "kv_heads": m.num_kv_heads, "head_dim": d,
                        "parallelism": f"kv-head sharded x{world}" if world > 1 else "1 GPU",
-                       "sharing": bool(args.sharing),
-                       "l2": "inputs larger than L2 (KV per layer > 126 MB), no flush"},
+                       "sharing": bool(args.sharing), "cuda_graph": bool(args.graph),
+                       "l2": "inputs larger than L2 (KV per layer > 126 MB), no flush"
+                       if dom["alg_bytes"] > 4 * 126e6 else "KV per layer fits L2: latency, not bandwidth"},
             "gpu_launches": int(launches_per_step * args.steps),
-            "layer_ms": layer_ms,
-            "layer_ms_isolated": layer_ms_isolated,
+            "layer_ms": dom["layer_ms"],
+            "layer_ms_isolated": dom["layer_ms_isolated"],
+            "per_window": {str(w): {k: v for k, v in pw.items() if k != "stats"} | {
+                "n_records": pw["stats"]["n_records"], "unique_tokens": pw["stats"]["unique_tokens"],
+                "gbs": pw["alg_bytes"] / (pw["layer_ms"] * 1e-3) / 1e9} for w, pw in per_window.items()},
             "hbm_gbs_algorithmic": achieved,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
                          "traffic_source": "profiles/latest_ncu.json (ncu dram__bytes_read+write per launch)",
-                         "kernel": ("decode_kernel + merge_kernel (one spa_decode_attention call)" if sep
-                                    else "decode_kernel (split merge in-kernel, tail phase)" if args.merge_mode == 0
-                                    else "decode_kernel (split merge in-kernel, last arriver)"),
-                         "peak_kind": pk_kind, "alg_bytes_per_launch": int(alg_bytes),
+                         "kernel": kname, "window": wdom,
+                         "peak_kind": pk_kind, "alg_bytes_per_launch": int(dom["alg_bytes"]),
                          "frac_of_8tbs": achieved / 8000.0,
                          "same_run_read_ceilings_gbs": ceilings,
                          "frac_of_tma_ceiling": (achieved / ceilings["tma_pool_read_gbs"]) if ceilings else None},
@@ -504,7 +607,6 @@ def run_reference(args):
     if rank != 0:
         return None
     recipe = recipe_for(args.config)
-    m = recipe.model
     ops, batch = workloads.call_log(recipe)
     budget = max(2.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
     vals = []
@@ -518,7 +620,7 @@ def run_reference(args):
     res = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step_ms, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": recipe.name, "n_requests": len(batch), "layers": m.num_layers},
+           "config": {"workload": f"{recipe.name} (BJ config {BJ_INDEX[args.config]})", "n_requests": len(batch)},
            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": info["cores"], "kind": "oracle",
                             "sample": info["sample"]},
            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

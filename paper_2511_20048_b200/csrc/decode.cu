@@ -40,7 +40,7 @@ struct DecodeParams {
     int layer_row_base;  // layer * num_pages * Hkv * 16
     int num_q_heads, group_size, num_kv_heads;
     int fused_merge;     // 0 merge kernel, 1 last arriver merges, 2 tail phase merges
-    int layer;           // selects this launch's work-queue counters
+    int launch;          // launch id since the plan was built: selects/owns a work-queue slot
 };
 
 constexpr int kDecodeWarps = 8;
@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(kDecodeWarps * 32, 1)
     const int32_t* pages = meta + meta[H_OFF_PAGES];
     const int32_t* rec_ptr = meta + meta[H_OFF_REC_PTR];
     int32_t* counters = const_cast<int32_t*>(meta) + meta[H_OFF_COUNTERS];
-    int32_t* sched = const_cast<int32_t*>(meta) + meta[H_OFF_SCHED] + 4 * p.layer;
+    int32_t* sched = const_cast<int32_t*>(meta) + meta[H_OFF_SCHED] + 4 * (p.launch % kSchedSlots);
     const int n_items = meta[H_N_ITEMS];
     const int G = p.group_size, Hq = p.num_q_heads, Hkv = p.num_kv_heads;
     uint64_t policy = 0;
@@ -151,7 +151,12 @@ __global__ void __launch_bounds__(kDecodeWarps * 32, 1)
         if (p_done) return;
         if (p_item < 0) {
             int qi = 0;
-            if (lane == 0) qi = atomicAdd(sched, 1);
+            if (lane == 0) {
+                if (p_n == 0)   // the slot is ours once launch - kSchedSlots rewound it (rarely waits)
+                    for (unsigned ns = 64; ld_acquire_gpu(sched + 3) != p.launch; ns = min(ns * 2, 1024u))
+                        __nanosleep(ns);
+                qi = atomicAdd(sched, 1);
+            }
             qi = __shfl_sync(0xffffffffu, qi, 0);
             const int it = qi < n_items ? queue[qi] : -1;
             if (lane == 0) tq[p_n % C::QN] = it;
@@ -561,6 +566,7 @@ __global__ void __launch_bounds__(kDecodeWarps * 32, 1)
             sched[0] = 0;
             sched[1] = 0;
             sched[2] = 0;
+            st_release_gpu(sched + 3, p.launch + kSchedSlots);   // hand the slot on
         }
     }
 }
@@ -607,7 +613,7 @@ int launch_decode(const spa_plan* P, int32_t layer, const void* q, int64_t q_sr,
     dp.num_kv_heads = c.num_kv_heads;
     dp.group_size = c.num_q_heads / c.num_kv_heads;
     dp.fused_merge = P->cfg.merge_mode == 0 ? 2 : P->cfg.merge_mode == 1 ? 1 : 0;
-    dp.layer = layer;
+    dp.launch = int(P->launches++);
     int err = 0;
     if (c.head_dim == 64)
         err = P->mt == 1 ? launch_decode_t<64, 1, 2>(P, dp, stream) : launch_decode_t<64, 2, 2>(P, dp, stream);

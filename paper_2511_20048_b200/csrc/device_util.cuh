@@ -88,6 +88,10 @@ __device__ __forceinline__ void red_add_release_gpu(int* addr, int v) {
     asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(addr), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ void st_release_gpu(int* addr, int v) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(addr), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ int ld_acquire_gpu(const int* addr) {
     int v;
     asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(addr) : "memory");

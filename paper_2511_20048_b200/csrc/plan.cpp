@@ -223,10 +223,13 @@ spa_status spa_decode_plan(spa_plan* P, int32_t n_req, const spa_req* reqs, int3
     // atomic each, so faster SMs take more work and the tail is made of the smallest items
     std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return cost(x) > cost(y); });
     const int T = P->n_teams;
-    // per layer: [0] next queue slot, [1] teams finished, [2] next tail-merge task (all
-    // self-resetting).  Per layer, so a layer's kernel may start popping while the previous
-    // layer's kernel drains (programmatic dependent launch).
-    const std::vector<int32_t> sched(size_t(pool->cfg.num_layers) * 4, 0);
+    // kSchedSlots slots of {queue head, teams finished, tail-merge head, owner}: launch i of
+    // this plan uses slot i % kSchedSlots once `owner` == i, so a launch may pop its queue
+    // while its predecessors (programmatic dependent launch) still drain; the last team of
+    // a launch rewinds the slot and hands it to launch i + kSchedSlots.
+    std::vector<int32_t> sched(size_t(kSchedSlots) * 4, 0);
+    for (int s = 0; s < kSchedSlots; ++s) sched[size_t(s) * 4 + 3] = s;
+    P->launches = 0;
 
     // tail-merge tasks (merge_mode 0): every (request with > 1 record, KV head), ordered
     // by the queue position of its last item, so the earliest-complete merges come first

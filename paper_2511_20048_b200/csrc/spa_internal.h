@@ -27,7 +27,7 @@ enum MetaHeader : int {
     H_OFF_DESC = 5,
     H_OFF_MEMBER = 6,
     H_OFF_ITEM = 7,
-    H_OFF_SCHED = 8,       // int32[L][4]: per layer queue head, finished teams, tail-merge head (reset in-kernel)
+    H_OFF_SCHED = 8,       // int32[kSchedSlots][4]: queue head, finished teams, tail-merge head, owner launch
     H_OFF_QUEUE = 9,       // int32[n_items]: item indices, largest first
     H_OFF_PAGES = 10,
     H_OFF_REC_PTR = 11,
@@ -63,6 +63,7 @@ constexpr int kPageSize = 16;          // tokens per page the kernels implement
 constexpr int kPagesPerStage = 2;      // pages of one (KV head) streamed per pipeline stage
 constexpr int kWarps = 4;              // warps per CTA of the decode kernel
 constexpr int kSmemBudget = 196 * 1024;
+constexpr int kSchedSlots = 4;         // work-queue counter slots per plan (launch i uses i % 4)
 
 // ---------------------------------------------------------------------------- pool
 struct Request {
@@ -113,6 +114,7 @@ struct spa_plan {
     spa_plan_stats stats{};
     int32_t window = 0;
     int32_t n_req = 0;
+    mutable int64_t launches = 0;  // decode launches since the last spa_decode_plan (queue slot owner ids)
 };
 
 struct spa_comm {
