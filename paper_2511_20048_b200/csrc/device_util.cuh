@@ -141,15 +141,15 @@ __device__ __forceinline__ void warp_merge_head(const float* part_o, const float
                                                 long long l_sh, int lane, int dim = DT) {
     const int D = DT ? DT : dim;
     orow += (long long)head * o_sh;
-    if (s1 - s0 <= 8 && D <= 128) {
-        // few records (the usual split count): issue the LSE loads and every partial O load
-        // back to back -- one L2 round trip -- then reduce in registers
+    if (s1 - s0 <= 16 && D <= 128) {
+        // few records (<= 2 x the automatic split cap): issue the LSE loads and every partial
+        // O load back to back -- one L2 round trip -- then reduce in registers
         const int S = s1 - s0;
         const int c = lane * 4;
         const float ls = lane < S ? __ldcg(part_lse + (long long)(s0 + lane) * H + head) : -INFINITY;
-        float4 v[8];
+        float4 v[16];
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
+        for (int j = 0; j < 16; ++j)
             v[j] = (j < S && c < D)
                        ? __ldcg(reinterpret_cast<const float4*>(part_o + ((long long)(s0 + j) * H + head) * D + c))
                        : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -163,7 +163,7 @@ __device__ __forceinline__ void warp_merge_head(const float* part_o, const float
         const float w = (ls != -INFINITY) ? expf(ls - lse) : 0.f;
         float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < 16; ++j) {
             const float wj = __shfl_sync(0xffffffffu, w, j);
             if (j < S && wj != 0.f) {
                 a.x += wj * v[j].x;

@@ -176,8 +176,11 @@ spa_status spa_decode_plan(spa_plan* P, int32_t n_req, const spa_req* reqs, int3
     int64_t pages_read = 0;
     for (const auto& r : ranges) {
         const int32_t pa = r.a / ps, pb = int32_t(cdiv(r.b, ps));
-        for (int32_t s = pa; s < pb; s += C) {
-            const int32_t e = std::min(pb, s + C);
+        // at most kMaxSplits splits per range: a request then has <= 2 kMaxSplits partial
+        // records (shared + tail), which the merge combines in one L2 round trip
+        const int32_t Cr = P->cfg.split_pages > 0 ? C : std::max<int32_t>(C, int32_t(cdiv(pb - pa, kMaxSplits)));
+        for (int32_t s = pa; s < pb; s += Cr) {
+            const int32_t e = std::min(pb, s + Cr);
             Desc d{};
             d.page_off = int32_t(pages.size());
             d.n_pages = e - s;

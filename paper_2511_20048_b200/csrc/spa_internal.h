@@ -64,6 +64,8 @@ constexpr int kPagesPerStage = 2;      // pages of one (KV head) streamed per pi
 constexpr int kWarps = 4;              // warps per CTA of the decode kernel
 constexpr int kSmemBudget = 196 * 1024;
 constexpr int kSchedSlots = 4;         // work-queue counter slots per plan (launch i uses i % 4)
+constexpr int kMaxSplits = 8;          // automatic splits per range (shared region or member tail)
+constexpr int kMergeFast = 16;         // records merged in one round trip (>= 2 kMaxSplits)
 
 // ---------------------------------------------------------------------------- pool
 struct Request {

@@ -311,3 +311,23 @@ def test_sharded_single_rank_layout():
     torch.cuda.synchronize()
     assert torch.equal(og.permute(1, 0, 2), o_ref) and torch.equal(lg.t(), l_ref)
     comm.close()
+
+
+@pytest.mark.timeout(120, method="thread")
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_back_to_back_launches_same_plan_and_layer(mode):
+    """Launches chained by programmatic dependent launch may start while the previous one
+    drains; repeating one (plan, layer) back to back must neither deadlock nor mix work
+    queues (each launch owns a queue slot by launch id)."""
+    rec = workloads.random_small(41, workloads.Model("m", 2, 8, 2, 128), max_prefix=600)
+    errs, outs, gb, plan, rp = run_parity(rec, "needle_shared_pos", split_pages=2, merge_mode=mode)
+    _assert_ok(errs)
+    q = bits_to_torch(gb.inputs.q[1]).contiguous()
+    N, Hq, d = q.shape
+    o = torch.empty((12, N, Hq, d), dtype=torch.bfloat16, device="cuda")
+    lse = torch.empty((12, N, Hq), dtype=torch.float32, device="cuda")
+    for i in range(12):                              # no synchronisation in between
+        plan.decode(1, q, o[i], lse[i], scale=rec.model.softmax_scale)
+    torch.cuda.synchronize()
+    for i in range(12):
+        assert torch.equal(o[i], outs[1][0]) and torch.equal(lse[i], outs[1][1])
