@@ -134,6 +134,9 @@ typedef struct spa_plan_config {
                                1: inside the decode kernel, by the last item of each (request, KV
                                  head) to finish;
                                2: by a separate merge_kernel launch (programmatic dependent launch) */
+    int32_t teams_per_cta;  /* work-item streams per CTA, each with a private shared-memory ring:
+                               4 (default for max_rows 16): 4 x 3-stage rings; 2: 2 x 6; 1: 1 x 12
+                               (deeper rings stream faster per item: small batches)              */
 } spa_plan_config;
 
 /* cfg may be NULL (defaults).  The plan keeps a pointer to `pool`. */

@@ -43,14 +43,14 @@ struct DecodeParams {
     int launch;          // launch id since the plan was built: selects/owns a work-queue slot
 };
 
-constexpr int kDecodeWarps = 8;
 constexpr int kSmemMax = 232448;   // 227 KB: the sm_100 per-block dynamic shared memory limit
 
-template <int D, int MT, int PPS>
+template <int D, int MT, int PPS, int TEAMS_>
 struct DecodeCfg {
     static constexpr int KW = 2;                          // key-split warps per row tile
     static constexpr int TEAM_WARPS = MT * KW;
-    static constexpr int TEAMS = kDecodeWarps / TEAM_WARPS;
+    static constexpr int TEAMS = TEAMS_;                  // teams (independent rings) per CTA
+    static constexpr int WARPS = TEAMS * TEAM_WARPS;
     static constexpr int PAGE_BYTES = kPageSize * D * 2;  // K (or V) of one page, one head
     static constexpr int STAGE_BYTES = PPS * 2 * PAGE_BYTES;
     // per (team, row tile): column-half exchange [2][16][D/2] fp32 + (m, l) [2][16][2]
@@ -77,11 +77,11 @@ struct DecodeCfg {
     static_assert(SMEM <= kSmemMax, "shared memory over the sm_100 limit");
 };
 
-template <int D, int MT, int PPS>
-__global__ void __launch_bounds__(kDecodeWarps * 32, 1)
+template <int D, int MT, int PPS, int TEAMS>
+__global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
     decode_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                   const DecodeParams p) {
-    using C = DecodeCfg<D, MT, PPS>;
+    using C = DecodeCfg<D, MT, PPS, TEAMS>;
     constexpr int KW = C::KW;
     constexpr int JW = PPS / KW;   // pages per warp per stage
     constexpr int KS = D / 16;     // k16 steps over the head dimension
@@ -571,23 +571,34 @@ __global__ void __launch_bounds__(kDecodeWarps * 32, 1)
     }
 }
 
-template <int D, int MT, int PPS>
+template <int D, int MT, int PPS, int TEAMS>
 static int launch_decode_t(const spa_plan* P, const DecodeParams& dp, void* stream) {
-    using C = DecodeCfg<D, MT, PPS>;
+    using C = DecodeCfg<D, MT, PPS, TEAMS>;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e =
-            cudaFuncSetAttribute(decode_kernel<D, MT, PPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaError_t e = cudaFuncSetAttribute(decode_kernel<D, MT, PPS, TEAMS>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
         if (e) return int(e);
         attr_set = true;
     }
     const CUtensorMap* tk = reinterpret_cast<const CUtensorMap*>(P->pool->tmap_k.bytes);
     const CUtensorMap* tv = reinterpret_cast<const CUtensorMap*>(P->pool->tmap_v.bytes);
-    return launch_pdl(decode_kernel<D, MT, PPS>, dim3(P->num_ctas), dim3(kDecodeWarps * 32), C::SMEM, stream, *tk,
-                      *tv, dp);
+    return launch_pdl(decode_kernel<D, MT, PPS, TEAMS>, dim3(P->num_ctas), dim3(C::WARPS * 32), C::SMEM, stream,
+                      *tk, *tv, dp);
 }
 
-int decode_teams_per_cta(int mt) { return kDecodeWarps / (mt * 2); }
+template <int D>
+static int launch_decode_d(const spa_plan* P, const DecodeParams& dp, void* stream) {
+    if (P->mt == 1) {
+        if (P->teams == 1) return launch_decode_t<D, 1, 2, 1>(P, dp, stream);
+        if (P->teams == 2) return launch_decode_t<D, 1, 2, 2>(P, dp, stream);
+        return launch_decode_t<D, 1, 2, 4>(P, dp, stream);
+    }
+    if (P->teams == 1) return launch_decode_t<D, 2, 2, 1>(P, dp, stream);
+    return launch_decode_t<D, 2, 2, 2>(P, dp, stream);
+}
+
+bool decode_teams_supported(int mt, int teams) { return teams == 1 || teams == 2 || (teams == 4 && mt == 1); }
 
 int launch_decode(const spa_plan* P, int32_t layer, const void* q, int64_t q_sr, int64_t q_sh, void* o, int64_t o_sr,
                   int64_t o_sh, float* lse, int64_t l_sr, int64_t l_sh, float scale, void* stream) {
@@ -615,10 +626,7 @@ int launch_decode(const spa_plan* P, int32_t layer, const void* q, int64_t q_sr,
     dp.fused_merge = P->cfg.merge_mode == 0 ? 2 : P->cfg.merge_mode == 1 ? 1 : 0;
     dp.launch = int(P->launches++);
     int err = 0;
-    if (c.head_dim == 64)
-        err = P->mt == 1 ? launch_decode_t<64, 1, 2>(P, dp, stream) : launch_decode_t<64, 2, 2>(P, dp, stream);
-    else
-        err = P->mt == 1 ? launch_decode_t<128, 1, 2>(P, dp, stream) : launch_decode_t<128, 2, 2>(P, dp, stream);
+    err = c.head_dim == 64 ? launch_decode_d<64>(P, dp, stream) : launch_decode_d<128>(P, dp, stream);
     if (err) return err;
     if (H[H_N_RECORDS] > 0 && !dp.fused_merge)
         err = launch_merge(H[H_N_REQ], c.num_q_heads, c.head_dim, P->d_meta + H[H_OFF_REC_PTR], P->d_part_o,

@@ -67,7 +67,15 @@ spa_status spa_plan_create(spa_pool* pool, const spa_plan_config* cfg, spa_plan*
     int ctas = c.num_ctas;
     if (ctas == 0) ctas = pool->sm_count > 0 ? pool->sm_count : 148;
     P->num_ctas = ctas;
-    P->n_teams = ctas * decode_teams_per_cta(P->mt);
+    int teams = c.teams_per_cta;
+    if (const char* e = std::getenv("SPA_TEAMS")) teams = std::atoi(e);
+    if (teams == 0) teams = P->mt == 1 ? 4 : 2;
+    if (!decode_teams_supported(P->mt, teams)) {
+        delete P;
+        return fail(SPA_ERR_UNSUPPORTED, "teams_per_cta must be 1, 2 or 4 (4 only with max_rows 16)");
+    }
+    P->teams = teams;
+    P->n_teams = ctas * teams;
     *out = P;
     return SPA_OK;
 }
@@ -178,7 +186,11 @@ spa_status spa_decode_plan(spa_plan* P, int32_t n_req, const spa_req* reqs, int3
         const int32_t pa = r.a / ps, pb = int32_t(cdiv(r.b, ps));
         // at most kMaxSplits splits per range: a request then has <= 2 kMaxSplits partial
         // records (shared + tail), which the merge combines in one L2 round trip
-        const int32_t Cr = P->cfg.split_pages > 0 ? C : std::max<int32_t>(C, int32_t(cdiv(pb - pa, kMaxSplits)));
+        // (small batches, C < cap_min: more splits keep every team streaming; merges are cheap)
+        static const int cap_min = std::getenv("SPA_SPLIT_CAP_MIN") ? std::atoi(std::getenv("SPA_SPLIT_CAP_MIN")) : 0;
+        const int32_t Cr = P->cfg.split_pages > 0 || C < cap_min
+                               ? C
+                               : std::max<int32_t>(C, int32_t(cdiv(pb - pa, kMaxSplits)));
         for (int32_t s = pa; s < pb; s += Cr) {
             const int32_t e = std::min(pb, s + Cr);
             Desc d{};

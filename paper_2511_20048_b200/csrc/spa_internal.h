@@ -98,6 +98,7 @@ struct spa_plan {
     spa_pool* pool = nullptr;
     spa_plan_config cfg{};
     int mt = 1;                 // m16 tiles (warps) per team: max_rows / 16
+    int teams = 4;              // teams (work-item streams with private rings) per CTA
     int n_teams = 0;
     int num_ctas = 0;
     // host view of the last plan
@@ -134,7 +135,7 @@ int launch_decode(const spa_plan* plan, int32_t layer, const void* q, int64_t q_
 int launch_merge(int32_t n_req, int32_t num_heads, int32_t head_dim, const int32_t* rec_ptr, const float* part_o,
                  const float* part_lse, void* o, int64_t o_sr, int64_t o_sh, float* lse, int64_t l_sr, int64_t l_sh,
                  int grid_hint, void* stream);
-int decode_teams_per_cta(int mt);   // decode.cu: work-item streams per CTA
+bool decode_teams_supported(int mt, int teams);   // decode.cu: compiled (row tiles, teams/CTA)
 int memset_pool(spa_pool* pool);
 bool make_tensor_maps(spa_pool* pool, std::string* err);
 int device_sm_count(int* device_out);

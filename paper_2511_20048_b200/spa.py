@@ -38,7 +38,7 @@ class spa_pool_config(ctypes.Structure):
 
 class spa_plan_config(ctypes.Structure):
     _fields_ = [("sharing", c_int32), ("max_rows", c_int32), ("split_pages", c_int32), ("num_ctas", c_int32),
-                ("merge_mode", c_int32)]
+                ("merge_mode", c_int32), ("teams_per_cta", c_int32)]
 
 
 class spa_plan_stats(ctypes.Structure):
@@ -285,10 +285,11 @@ class Pool:
 
 
 class Plan:
-    def __init__(self, pool: Pool, sharing=True, max_rows=16, split_pages=0, num_ctas=0, merge_mode=0):
+    def __init__(self, pool: Pool, sharing=True, max_rows=16, split_pages=0, num_ctas=0, merge_mode=0,
+                 teams_per_cta=0):
         """merge_mode: 0 in-kernel tail phase (default), 1 in-kernel last arriver, 2 merge kernel."""
         self.pool = pool
-        cfg = spa_plan_config(1 if sharing else 0, max_rows, split_pages, num_ctas, int(merge_mode))
+        cfg = spa_plan_config(1 if sharing else 0, max_rows, split_pages, num_ctas, int(merge_mode), int(teams_per_cta))
         h = c_void_p()
         _check(lib().spa_plan_create(pool.h, ctypes.byref(cfg), ctypes.byref(h)))
         self.h = h
