@@ -49,6 +49,21 @@ spa_status spa_plan_debug_array(const spa_plan* plan, int32_t which, const int32
 spa_status spa_debug_read_bw_ldg(const void* buf, size_t bytes, void* sink4, void* stream);
 spa_status spa_debug_pool_read_tma(const spa_pool* pool, int32_t layers, int32_t mode, void* stream);
 
+/* Timeline trace of the decode kernel (performance analysis only).  While set, every
+ * spa_decode_attention launch of `plan` writes, per warp (CTA-major), up to `cap` events of
+ * 2 uint64 each into the caller-owned device buffer `buf`
+ * (num_ctas * warps_per_cta * cap * 16 bytes, from spa_debug_plan_geometry):
+ *   word 0: %globaltimer (ns, device-wide)
+ *   word 1: (tag << 56) | (item or subtask & 0xffffff) << 32 | (clock64 & 0xffffffff)
+ * tags: 1 kernel entry, 2 item start (first stage landed), 3 item end (output written),
+ *       8 item's partial records counted in (in-kernel merge), 4 tail-merge subtask popped,
+ *       7 its records complete, 5 subtask merged, 6 warp leaves the kernel.
+ * Slots past a warp's last event are left untouched (zero the buffer first).  buf = NULL
+ * turns tracing off.  Each launch overwrites the buffer. */
+spa_status spa_debug_set_trace(spa_plan* plan, void* buf, int32_t cap);
+spa_status spa_debug_plan_geometry(const spa_plan* plan, int32_t* out_num_ctas, int32_t* out_teams_per_cta,
+                                   int32_t* out_warps_per_cta);
+
 #ifdef __cplusplus
 }
 #endif

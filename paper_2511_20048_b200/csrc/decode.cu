@@ -22,10 +22,6 @@
 
 namespace spa {
 
-int launch_merge(int32_t n_req, int32_t num_heads, int32_t head_dim, const int32_t* rec_ptr, const float* part_o,
-                 const float* part_lse, void* o, int64_t o_sr, int64_t o_sh, float* lse, int64_t l_sr, int64_t l_sh,
-                 int grid_hint, void* stream);
-
 struct DecodeParams {
     const int32_t* meta;
     const __nv_bfloat16* q;
@@ -41,6 +37,15 @@ struct DecodeParams {
     int num_q_heads, group_size, num_kv_heads;
     int fused_merge;     // 0 merge kernel, 1 last arriver merges, 2 tail phase merges
     int launch;          // launch id since the plan was built: selects/owns a work-queue slot
+    unsigned long long* trace;   // spa_debug_set_trace timeline (null: off)
+    int trace_cap;
+    unsigned poll_min, poll_max;   // tail-merge polling backoff (ns)
+};
+
+// A popped work item as the producer hands it to its team (shared memory): the item and
+// the descriptor fields the consumers need, so they do not re-read them from global memory.
+struct TeamItem {
+    int it, kv_head, n_pages, tok_start, tok_end, member_off, n_members, pad;
 };
 
 constexpr int kSmemMax = 232448;   // 227 KB: the sm_100 per-block dynamic shared memory limit
@@ -56,7 +61,7 @@ struct DecodeCfg {
     // per (team, row tile): column-half exchange [2][16][D/2] fp32 + (m, l) [2][16][2]
     static constexpr int COMB_BYTES = TEAMS * MT * (2 * 16 * (D / 2) * 4 + 2 * 16 * 2 * 4);
     // barriers (full + empty), the team mailbox and the popped-item queue, for n stages
-    static constexpr int misc(int n) { return TEAMS * n * 2 * 8 + TEAMS * 4 + TEAMS * (n + 2) * 4 + 16; }
+    static constexpr int misc(int n) { return TEAMS * n * 2 * 8 + TEAMS * 4 + TEAMS * (n + 2) * 32 + 16; }
     static constexpr int max_stages() {
         int n = 1;
         while (1024 + (n + 1) * TEAMS * STAGE_BYTES + misc(n + 1) + COMB_BYTES <= kSmemMax) ++n;
@@ -69,9 +74,9 @@ struct DecodeCfg {
     static constexpr int OFF_BARS = RING_BYTES;
     static constexpr int OFF_SLOT = OFF_BARS + TEAMS * NS * 2 * 8;
     static constexpr int OFF_TQ = OFF_SLOT + TEAMS * 4;
-    static constexpr int OFF_COMB = (OFF_TQ + TEAMS * QN * 4 + 15) & ~15;
+    static constexpr int OFF_COMB = (OFF_TQ + TEAMS * QN * 32 + 15) & ~15;
     static constexpr int SMEM = 1024 + OFF_COMB + COMB_BYTES;
-    static_assert(NS >= 2, "pipeline needs >= 2 stages");
+    static_assert(NS >= 2 && (TEAMS < 4 || NS >= 3), "pipeline needs >= 2 stages (3 with 4 teams)");
     static_assert(PPS % KW == 0, "each key-split warp takes whole pages");
     static_assert(OFF_COMB - OFF_BARS <= MISC_BYTES, "misc shared-memory region too small");
     static_assert(SMEM <= kSmemMax, "shared memory over the sm_100 limit");
@@ -101,7 +106,7 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
     auto full_bar = [&](int s) { return bars + (team * C::NS + s) * 8; };
     auto empty_bar = [&](int s) { return bars + (C::TEAMS * C::NS + team * C::NS + s) * 8; };
     uint32_t* team_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_SLOT) + team;
-    int32_t* tq = reinterpret_cast<int32_t*>(smem + C::OFF_TQ) + team * C::QN;
+    TeamItem* tq = reinterpret_cast<TeamItem*>(smem + C::OFF_TQ) + team * C::QN;
     float* comb = reinterpret_cast<float*>(smem + C::OFF_COMB) + (team * MT + wt) * (2 * 16 * (D / 2) + 2 * 16 * 2);
     float* ml = comb + 2 * 16 * (D / 2);
     auto team_sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(C::TEAM_WARPS * 32) : "memory"); };
@@ -124,6 +129,22 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
     // merge counters are touched after the wait.
     asm volatile("griddepcontrol.launch_dependents;");
 
+    // timeline trace (spa_debug_set_trace): lane 0 of every warp records events
+    unsigned long long* trace =
+        p.trace ? p.trace + 2ull * (blockIdx.x * C::WARPS + warp) * p.trace_cap : nullptr;
+    int tr_n = 0;
+    auto tr = [&](unsigned long long tag, int id) {
+        if (trace && lane == 0 && tr_n < p.trace_cap) {
+            unsigned long long gt, ck;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+            asm volatile("mov.u64 %0, %%clock64;" : "=l"(ck));
+            trace[2 * tr_n] = gt;
+            trace[2 * tr_n + 1] = (tag << 56) | ((unsigned long long)(id & 0xffffff) << 32) | (ck & 0xffffffffull);
+            ++tr_n;
+        }
+    };
+    tr(1, 0);
+
     const int32_t* meta = p.meta;
     const Desc* descs = reinterpret_cast<const Desc*>(meta + meta[H_OFF_DESC]);
     const Member* mems = reinterpret_cast<const Member*>(meta + meta[H_OFF_MEMBER]);
@@ -132,7 +153,7 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
     const int32_t* pages = meta + meta[H_OFF_PAGES];
     const int32_t* rec_ptr = meta + meta[H_OFF_REC_PTR];
     int32_t* counters = const_cast<int32_t*>(meta) + meta[H_OFF_COUNTERS];
-    int32_t* sched = const_cast<int32_t*>(meta) + meta[H_OFF_SCHED] + 4 * (p.launch % kSchedSlots);
+    int32_t* sched = const_cast<int32_t*>(meta) + meta[H_OFF_SCHED] + kSchedStride * (p.launch % kSchedSlots);
     const int n_items = meta[H_N_ITEMS];
     const int G = p.group_size, Hq = p.num_q_heads, Hkv = p.num_kv_heads;
     uint64_t policy = 0;
@@ -159,17 +180,22 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
             }
             qi = __shfl_sync(0xffffffffu, qi, 0);
             const int it = qi < n_items ? queue[qi] : -1;
-            if (lane == 0) tq[p_n % C::QN] = it;
+            TeamItem* e = &tq[p_n % C::QN];
             ++p_n;
             if (it < 0) {
                 p_done = true;
-                if (lane == 0) mbar_arrive(full_bar(slot));
+                if (lane == 0) {
+                    e->it = -1;
+                    mbar_arrive(full_bar(slot));
+                }
                 return;
             }
             p_item = it;
             p_st = 0;
             const Item itm = items[it];
             const Desc dsc = descs[itm.desc];
+            if (lane == 0) *e = TeamItem{it, itm.kv_head, dsc.n_pages, dsc.tok_start, dsc.tok_end, dsc.member_off,
+                                         dsc.n_members, 0};
             if ((dsc.kind & 4) && !p_waited) {   // holds a newest token: wait for its producer
                 asm volatile("griddepcontrol.wait;" ::: "memory");
                 p_waited = true;
@@ -218,14 +244,35 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
 
     int slot = 0, c_n = 0;
     uint32_t phase = 0;
+    // deferred record counting of the tail merge (fused_merge 2): the last item's members
+    int pend_moff = 0, pend_nm = 0, pend_kv = 0;
+    auto count_records = [&]() {   // producer warp; the other warp's stores are ordered before
+        if (pend_nm > 0 && lane == 0) {
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            for (int mb = 0; mb < pend_nm; ++mb) {
+                const Member mm = mems[pend_moff + mb];
+                if (mm.rec >= 0)
+                    asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(counters + mm.row * Hkv + pend_kv)
+                                 : "memory");
+            }
+        }
+        pend_nm = 0;
+    };
     while (true) {
         // the first stage of the next item (or the end-of-queue marker) has landed
         mbar_wait(full_bar(slot), phase);
-        const int it = tq[c_n % C::QN];
+        const TeamItem dsc = tq[c_n % C::QN];
+        const int it = dsc.it;
         ++c_n;
-        if (it < 0) break;
-        const Item itm = items[it];
-        const Desc dsc = descs[itm.desc];
+        if (it < 0) {
+            if (p.fused_merge == 2) {   // the last item's records: order both warps' stores first
+                team_sync();
+                if (producer) count_records();
+            }
+            break;
+        }
+        tr(2, it);
+        const TeamItem& itm = dsc;
         const int R = dsc.n_members * G;
         const bool active = wt * 16 < R;   // identical for the KW warps of a row tile
         const int row0 = wt * 16 + (lane >> 2), row1 = row0 + 8;
@@ -398,7 +445,11 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(empty_bar(slot));
             if (producer) {
-                mbar_wait(empty_bar(slot), phase);
+                mbar_wait(empty_bar(slot), phase);   // acquire: both warps are past the stage
+                if (pend_nm) {
+                    count_records();
+                    tr(8, 0);
+                }
                 issue_next(slot);
             }
             if (++slot == C::NS) {
@@ -489,20 +540,21 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
             }
         }
 
+        tr(3, it);
         // ---- in-kernel split merge (fused_merge 1 / 2)
         bool any_partial = false;
         for (int mb = 0; mb < dsc.n_members; ++mb) any_partial |= mems[dsc.member_off + mb].rec >= 0;
         if (any_partial && p.fused_merge == 2) {
-            // tail merge: count this item's records in (release); merged after the queue
-            team_sync();
-            if (producer && lane == 0)
-                for (int mb = 0; mb < dsc.n_members; ++mb) {
-                    const Member mm = mems[dsc.member_off + mb];
-                    if (mm.rec >= 0) red_add_release_gpu(counters + mm.row * Hkv + itm.kv_head, 1);
-                }
+            // tail merge: this item's records are counted in (release) by the producer once
+            // both warps have released the next stage -- off the item-to-item critical path
+            pend_moff = dsc.member_off;
+            pend_nm = dsc.n_members;
+            pend_kv = itm.kv_head;
         } else if (any_partial && p.fused_merge == 1) {
             // the team barrier orders every lane's partial stores before the producer lane's
-            // acq_rel arrival (release is cumulative); the last arriver acquires all of them
+            // acq_rel arrival (release is cumulative); the last arriver acquires all of them.
+            // Counters are never reset: launch k of the plan completes a (row, head) at
+            // (k + 1) x its record count (the plan upload zeroes them).
             team_sync();
             uint32_t mask = 0;
             if (producer && lane == 0) {
@@ -511,10 +563,7 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
                     if (mm.rec < 0) continue;
                     const int nrec = rec_ptr[mm.row + 1] - rec_ptr[mm.row];
                     int* c = counters + mm.row * Hkv + itm.kv_head;
-                    if (atom_add_acq_rel_gpu(c, 1) == nrec - 1) {
-                        mask |= 1u << mb;
-                        *c = 0;    // every arrival of this launch is in: ready for the next layer
-                    }
+                    if (atom_add_acq_rel_gpu(c, 1) == (p.launch + 1) * nrec - 1) mask |= 1u << mb;
                 }
                 *team_slot = mask;
             }
@@ -525,47 +574,58 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
                 const int mb = __ffs(mask) - 1;
                 mask &= mask - 1;
                 const Member mm = mems[dsc.member_off + mb];
+                const int s0 = rec_ptr[mm.row], s1 = rec_ptr[mm.row + 1];
+                __nv_bfloat16* orow = p.o + mm.row * p.o_sr;
+                float* lrow = p.lse ? p.lse + mm.row * p.l_sr : nullptr;
                 for (int hh = tw; hh < G; hh += C::TEAM_WARPS)
-                    warp_merge_head<D>(p.part_o, p.part_lse, Hq, rec_ptr[mm.row], rec_ptr[mm.row + 1],
-                                       itm.kv_head * G + hh, p.o + mm.row * p.o_sr, p.o_sh,
-                                       p.lse ? p.lse + mm.row * p.l_sr : nullptr, p.l_sh, lane);
+                    warp_merge_head<D>(p.part_o, p.part_lse, Hq, s0, s1, itm.kv_head * G + hh, orow, p.o_sh, lrow,
+                                       p.l_sh, lane);
             }
         }
     }
 
-    // ---- tail merge (fused_merge == 2): every item has been popped; teams now pop merge
-    //      tasks (request, KV head), wait until all of the task's records are counted in
-    //      (acquire; the items still running are owned by teams not in this loop), merge.
+    // ---- tail merge (fused_merge == 2): every item has been popped; each WARP now pops
+    //      merge subtasks -- a whole (request, KV head) task when G x S <= 32 (one warp,
+    //      warp_merge_group), else one head of it -- waits until all of the task's records of
+    //      this launch are counted in (every lane acquires; the items still running are owned
+    //      by teams not in this loop), and merges.  Counters are never reset: launch k of the
+    //      plan completes a task at (k + 1) x its record count.  One queue, popped in the
+    //      plan's earliest-ready order.
     if (p.fused_merge == 2) {
-        const int32_t* mtask = meta + meta[H_OFF_MTASK];
-        const int n_mtask = meta[H_N_MTASK];
+        const int32_t* msub = meta + meta[H_OFF_MTASK];
+        const int n_sub = meta[H_N_MTASK];
+        int* qhead = sched + 32;   // own 128-B line
         while (true) {
-            team_sync();
-            if (producer && lane == 0) *team_slot = uint32_t(atomicAdd(sched + 2, 1));
-            team_sync();
-            const int t = int(*team_slot);
-            if (t >= n_mtask) break;
-            const int task = mtask[t];
+            int t = 0;
+            if (lane == 0) t = atomicAdd(qhead, 1);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            if (t >= n_sub) break;
+            const int code = msub[t];
+            const int task = code >> 6, sub = code & 63;
+            tr(4, t);
             const int row = task / Hkv, g = task - row * Hkv;
             const int s0 = rec_ptr[row], s1 = rec_ptr[row + 1];
-            if (producer && lane == 0) {
-                int* c = counters + task;
-                // exponential backoff keeps hundreds of waiting teams off the L2 atomics
-                for (unsigned ns = 128; ld_acquire_gpu(c) < s1 - s0; ns = min(ns * 2, 2048u)) __nanosleep(ns);
-                *c = 0;   // all arrivals of this launch are in
-            }
-            team_sync();
-            for (int hh = tw; hh < G; hh += C::TEAM_WARPS)
-                warp_merge_head<D>(p.part_o, p.part_lse, Hq, s0, s1, g * G + hh, p.o + row * p.o_sr, p.o_sh,
-                                   p.lse ? p.lse + row * p.l_sr : nullptr, p.l_sh, lane);
+            const int target = (p.launch + 1) * (s1 - s0);
+            const int* c = counters + task;
+            for (unsigned ns = p.poll_min; ld_acquire_gpu(c) < target; ns = min(ns * 2, p.poll_max)) __nanosleep(ns);
+            tr(7, t);
+            __nv_bfloat16* orow = p.o + row * p.o_sr;
+            float* lrow = p.lse ? p.lse + row * p.l_sr : nullptr;
+            if (sub == 0)
+                warp_merge_group<D>(p.part_o, p.part_lse, Hq, s0, s1, g * G, G, orow, p.o_sh, lrow, p.l_sh, lane);
+            else
+                warp_merge_head<D>(p.part_o, p.part_lse, Hq, s0, s1, g * G + sub - 1, orow, p.o_sh, lrow, p.l_sh, lane);
+            tr(5, t);
         }
     }
-    // the last team to finish rewinds the queues for the next launch (stream-ordered)
-    if (producer && lane == 0) {
-        if (atomicAdd(sched + 1, 1) == int(gridDim.x) * C::TEAMS - 1) {
+    tr(6, 0);
+    // the last CTA to finish rewinds the queues for the next launch (stream-ordered)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (atomicAdd(sched + 1, 1) == int(gridDim.x) - 1) {
             sched[0] = 0;
             sched[1] = 0;
-            sched[2] = 0;
+            sched[32] = 0;
             st_release_gpu(sched + 3, p.launch + kSchedSlots);   // hand the slot on
         }
     }
@@ -625,6 +685,12 @@ int launch_decode(const spa_plan* P, int32_t layer, const void* q, int64_t q_sr,
     dp.group_size = c.num_q_heads / c.num_kv_heads;
     dp.fused_merge = P->cfg.merge_mode == 0 ? 2 : P->cfg.merge_mode == 1 ? 1 : 0;
     dp.launch = int(P->launches++);
+    dp.trace = P->trace;
+    dp.trace_cap = P->trace_cap;
+    static const unsigned poll_min = std::getenv("SPA_POLL_MIN") ? unsigned(std::atoi(std::getenv("SPA_POLL_MIN"))) : 32u;
+    static const unsigned poll_max = std::getenv("SPA_POLL_MAX") ? unsigned(std::atoi(std::getenv("SPA_POLL_MAX"))) : 256u;
+    dp.poll_min = poll_min;
+    dp.poll_max = poll_max;
     int err = 0;
     err = c.head_dim == 64 ? launch_decode_d<64>(P, dp, stream) : launch_decode_d<128>(P, dp, stream);
     if (err) return err;

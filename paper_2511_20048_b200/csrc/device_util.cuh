@@ -128,6 +128,83 @@ static int launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sm
     return int(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 
+// Merge the split partials of G <= 8 consecutive heads [head0, head0 + G) of one request
+// row, G x S <= 32 (S = s1 - s0 <= 16 records), D <= 128, in one warp pass: the LSEs of all
+// G heads and the float4 columns [4 lane, 4 lane + 4) of all G x S partial rows are loaded
+// back to back (one L2 round trip).  Per head the arithmetic (butterfly max and sum over
+// lanes j < S, FMAs in record order) is that of warp_merge_head's S <= 16 path, so a head
+// merged alone or within its group gets the same bits.
+template <int DT>
+__device__ __forceinline__ void warp_merge_group_small(const float* part_o, const float* part_lse, int H, int s0, int s1,
+                                                       int head0, int G, __nv_bfloat16* orow, long long o_sh,
+                                                       float* lrow, long long l_sh, int lane, int dim = DT) {
+    const int D = DT ? DT : dim;
+    const int S = s1 - s0, GS = G * S;
+    const int c = lane * 4;
+    // every LSE (lane j < S holds record j of head hh in ls[hh]) and every partial row
+    // (head-major, record-minor: v[hh * S + j]) in flight together
+    float ls[8];
+#pragma unroll
+    for (int hh = 0; hh < 8; ++hh)
+        ls[hh] = (hh < G && lane < S) ? __ldcg(part_lse + (long long)(s0 + lane) * H + head0 + hh) : -INFINITY;
+    const long long rs = (long long)H * D;
+    const float* pj = part_o + ((long long)s0 * H + head0) * D + c;
+    float4 v[32];
+    int jr = 0;
+#pragma unroll
+    for (int idx = 0; idx < 32; ++idx) {
+        v[idx] = (idx < GS && c < D) ? __ldcg(reinterpret_cast<const float4*>(pj)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        pj += rs;
+        if (++jr == S) {
+            jr = 0;
+            pj += D - S * rs;
+        }
+    }
+    // per head: warp_merge_head's reduction; the weight of (hh, j) moves to lane hh * S + j
+    float wflat = 0.f;
+#pragma unroll
+    for (int hh = 0; hh < 8; ++hh) {
+        if (hh < G) {
+            float m = ls[hh];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            float e = (ls[hh] != -INFINITY) ? expf(ls[hh] - m) : 0.f;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+            const float lse = (m == -INFINITY) ? -INFINITY : m + logf(e);
+            const float w = (ls[hh] != -INFINITY) ? expf(ls[hh] - lse) : 0.f;
+            const int src = lane - hh * S;
+            const float wm = __shfl_sync(0xffffffffu, w, src & 31);
+            if (src >= 0 && src < S) wflat = wm;
+            if (lane == 0 && lrow) lrow[(long long)(head0 + hh) * l_sh] = lse;
+        }
+    }
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    int jj = 0, hc = 0;
+#pragma unroll
+    for (int idx = 0; idx < 32; ++idx) {
+        if (idx < GS) {
+            const float wj = __shfl_sync(0xffffffffu, wflat, idx);
+            if (wj != 0.f) {
+                a.x += wj * v[idx].x;
+                a.y += wj * v[idx].y;
+                a.z += wj * v[idx].z;
+                a.w += wj * v[idx].w;
+            }
+            if (++jj == S) {
+                if (c < D) {
+                    __nv_bfloat16* op = orow + (long long)(head0 + hc) * o_sh + c;
+                    *reinterpret_cast<__nv_bfloat162*>(op) = __floats2bfloat162_rn(a.x, a.y);
+                    *reinterpret_cast<__nv_bfloat162*>(op + 2) = __floats2bfloat162_rn(a.z, a.w);
+                }
+                a = make_float4(0.f, 0.f, 0.f, 0.f);
+                jj = 0;
+                ++hc;
+            }
+        }
+    }
+}
+
 // ============================================================================ a6 core: one warp merges one head
 // Split-KV partial-LSE merge of records [s0, s1) of one (request, head) (oracle:
 // merge_partials; include/spa.h spa_merge_splits):
@@ -142,8 +219,9 @@ __device__ __forceinline__ void warp_merge_head(const float* part_o, const float
     const int D = DT ? DT : dim;
     orow += (long long)head * o_sh;
     if (s1 - s0 <= 16 && D <= 128) {
-        // few records (<= 2 x the automatic split cap): issue the LSE loads and every partial
-        // O load back to back -- one L2 round trip -- then reduce in registers
+        // few records: issue the LSE loads and every partial O load back to back (one L2
+        // round trip), then reduce in registers (warp_merge_group_small repeats this
+        // arithmetic per head, so both give the same bits)
         const int S = s1 - s0;
         const int c = lane * 4;
         const float ls = lane < S ? __ldcg(part_lse + (long long)(s0 + lane) * H + head) : -INFINITY;
@@ -164,12 +242,14 @@ __device__ __forceinline__ void warp_merge_head(const float* part_o, const float
         float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-            const float wj = __shfl_sync(0xffffffffu, w, j);
-            if (j < S && wj != 0.f) {
-                a.x += wj * v[j].x;
-                a.y += wj * v[j].y;
-                a.z += wj * v[j].z;
-                a.w += wj * v[j].w;
+            if (j < S) {
+                const float wj = __shfl_sync(0xffffffffu, w, j);
+                if (wj != 0.f) {
+                    a.x += wj * v[j].x;
+                    a.y += wj * v[j].y;
+                    a.z += wj * v[j].z;
+                    a.w += wj * v[j].w;
+                }
             }
         }
         if (c < D) {
@@ -179,37 +259,51 @@ __device__ __forceinline__ void warp_merge_head(const float* part_o, const float
         if (lane == 0 && lrow) lrow[(long long)head * l_sh] = lse;
         return;
     }
-    if (s1 - s0 <= 32) {
-        // common case: one record per lane, the LSEs are read once (one L2 round trip for
-        // the LSEs, one for the partial O rows, issued back to back)
+    if (s1 - s0 <= 128 && D <= 128) {
+        // up to 128 records: every LSE in one round trip (4 per lane), then the partial O rows
+        // in chunks of 16 records, each chunk's loads issued back to back (one round trip each)
         const int S = s1 - s0;
-        const float ls = lane < S ? __ldcg(part_lse + (long long)(s0 + lane) * H + head) : -INFINITY;
-        float m = ls;
+        const int c = lane * 4;
+        float ls[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            ls[k] = lane + 32 * k < S ? __ldcg(part_lse + (long long)(s0 + lane + 32 * k) * H + head) : -INFINITY;
+        float m = fmaxf(fmaxf(ls[0], ls[1]), fmaxf(ls[2], ls[3]));
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-        float e = (ls != -INFINITY) ? expf(ls - m) : 0.f;
+        float e = 0.f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) e += (ls[k] != -INFINITY) ? expf(ls[k] - m) : 0.f;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
         const float lse = (m == -INFINITY) ? -INFINITY : m + logf(e);
-        const float w = (ls != -INFINITY) ? expf(ls - lse) : 0.f;
-        for (int c = lane * 4; c - lane * 4 < D; c += 128) {
-            float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 8
-            for (int j = 0; j < S; ++j) {
-                const float wj = __shfl_sync(0xffffffffu, w, j);
-                if (c < D && wj != 0.f) {
-                    const float4 v =
-                        __ldcg(reinterpret_cast<const float4*>(part_o + ((long long)(s0 + j) * H + head) * D + c));
-                    a.x += wj * v.x;
-                    a.y += wj * v.y;
-                    a.z += wj * v.z;
-                    a.w += wj * v.w;
+        float w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) w[k] = (ls[k] != -INFINITY) ? expf(ls[k] - lse) : 0.f;
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int cb = 0; cb < S; cb += 16) {
+            float4 v[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                v[j] = (cb + j < S && c < D)
+                           ? __ldcg(reinterpret_cast<const float4*>(part_o + ((long long)(s0 + cb + j) * H + head) * D + c))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+            const int k = cb >> 5;
+            const float wk = k == 0 ? w[0] : k == 1 ? w[1] : k == 2 ? w[2] : w[3];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const float wj = __shfl_sync(0xffffffffu, wk, (cb & 31) + j);
+                if (cb + j < S && wj != 0.f) {
+                    a.x += wj * v[j].x;
+                    a.y += wj * v[j].y;
+                    a.z += wj * v[j].z;
+                    a.w += wj * v[j].w;
                 }
             }
-            if (c < D) {
-                *reinterpret_cast<__nv_bfloat162*>(orow + c) = __floats2bfloat162_rn(a.x, a.y);
-                *reinterpret_cast<__nv_bfloat162*>(orow + c + 2) = __floats2bfloat162_rn(a.z, a.w);
-            }
+        }
+        if (c < D) {
+            *reinterpret_cast<__nv_bfloat162*>(orow + c) = __floats2bfloat162_rn(a.x, a.y);
+            *reinterpret_cast<__nv_bfloat162*>(orow + c + 2) = __floats2bfloat162_rn(a.z, a.w);
         }
         if (lane == 0 && lrow) lrow[(long long)head * l_sh] = lse;
         return;
@@ -264,6 +358,22 @@ __device__ __forceinline__ void warp_merge_head(const float* part_o, const float
         }
     }
     if (lane == 0 && lrow) lrow[(long long)head * l_sh] = lse;
+}
+
+// Merge heads [head0, head0 + G) of one request row: all G in one warp pass when
+// G x S <= 32, else head by head (warp_merge_head).  Bit-identical to merging each head
+// alone with warp_merge_head, so every merge mode and path of the library agrees bitwise.
+template <int DT>
+__device__ __forceinline__ void warp_merge_group(const float* part_o, const float* part_lse, int H, int s0, int s1,
+                                                 int head0, int G, __nv_bfloat16* orow, long long o_sh, float* lrow,
+                                                 long long l_sh, int lane, int dim = DT) {
+    const int D = DT ? DT : dim;
+    if (G <= 8 && G * (s1 - s0) <= 32 && s1 - s0 <= 16 && D <= 128) {
+        warp_merge_group_small<DT>(part_o, part_lse, H, s0, s1, head0, G, orow, o_sh, lrow, l_sh, lane, dim);
+        return;
+    }
+    for (int hh = 0; hh < G; ++hh)
+        warp_merge_head<DT>(part_o, part_lse, H, s0, s1, head0 + hh, orow, o_sh, lrow, l_sh, lane, dim);
 }
 
 }  // namespace spa

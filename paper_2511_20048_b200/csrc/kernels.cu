@@ -179,7 +179,7 @@ struct MergeParams {
 };
 
 // One warp per (request, head); lanes stride over float4 columns.
-__global__ void __launch_bounds__(256) merge_kernel(const MergeParams p) {
+__global__ void __launch_bounds__(256, 1) merge_kernel(const MergeParams p) {
     asm volatile("griddepcontrol.wait;" ::: "memory");   // partials come from the decode kernel
     asm volatile("griddepcontrol.launch_dependents;");
     const int warps = (gridDim.x * blockDim.x) >> 5;

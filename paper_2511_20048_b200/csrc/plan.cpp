@@ -167,12 +167,58 @@ spa_status spa_decode_plan(spa_plan* P, int32_t n_req, const spa_req* reqs, int3
         unique_tokens += r.b - r.a;
         total_pages += cdiv(r.b, ps) - r.a / ps;
     }
+    static const int max_splits =
+        std::getenv("SPA_MAX_SPLITS") ? std::max(1, std::atoi(std::getenv("SPA_MAX_SPLITS"))) : kMaxSplits;
     int32_t C = P->cfg.split_pages;
     if (C <= 0) {
-        double div = 1.0;
-        if (const char* e = std::getenv("SPA_SPLIT_DIV")) div = std::max(0.25, std::atof(e));
         const double target = double(total_pages * Hkv) / double(std::max(1, P->n_teams));
-        C = int32_t(std::ceil(target / div));
+        if (const char* e = std::getenv("SPA_SPLIT_DIV")) {
+            C = int32_t(std::ceil(target / std::max(0.25, std::atof(e))));
+        } else {
+            // choose the split size whose work items the kernel's dynamic largest-first queue
+            // packs best onto n_teams teams: simulate list scheduling in LPT order (all teams
+            // equally fast) and add the cost of the fp32 partial records the splits create.
+            // Costs are in page units; an item costs its pages + 1 (pipeline refill + epilogue),
+            // a partial record of R rows R / 16 pages written + read, and any merge a fixed
+            // latency (~5 pages of one team's streaming).
+            const double fs[] = {1.0, 1.5, 2.0, 3.0, 4.0};
+            double best = 0;
+            std::vector<double> costs;
+            for (double f : fs) {
+                const int32_t Cf = std::max<int32_t>(4, int32_t(std::ceil(target / f)));
+                costs.clear();
+                double rec_pages = 0;
+                for (const auto& r : ranges) {
+                    const int32_t pa = r.a / ps, pb = int32_t(cdiv(r.b, ps));
+                    const int32_t Cr = std::max<int32_t>(Cf, int32_t(cdiv(pb - pa, max_splits)));
+                    const int32_t n = int32_t(cdiv(pb - pa, Cr));
+                    const double rows = double(r.members.size() * G);
+                    for (int32_t s = 0; s < n; ++s) {
+                        const int32_t np = std::min(Cr, pb - pa - s * Cr);
+                        const double c = np + 1 + (n > 1 || r.kind ? rows / 16.0 : 0.0);
+                        for (int h = 0; h < Hkv; ++h) costs.push_back(c);
+                    }
+                    if (n > 1) rec_pages += n * rows / 16.0 * Hkv;
+                }
+                if (costs.size() > 50000) continue;
+                std::sort(costs.begin(), costs.end(), std::greater<double>());
+                std::priority_queue<double, std::vector<double>, std::greater<double>> q;
+                for (int t = 0; t < P->n_teams; ++t) q.push(0.0);
+                double makespan = 0;
+                for (double c : costs) {
+                    const double t0 = q.top();
+                    q.pop();
+                    q.push(t0 + c);
+                    makespan = std::max(makespan, t0 + c);
+                }
+                const double score = makespan + rec_pages / P->n_teams + (rec_pages > 0 ? 5.0 : 0.0);
+                if (C <= 0 || score < best * 0.98) {   // prefer fewer splits unless clearly better
+                    best = score;
+                    C = Cf;
+                }
+            }
+            if (C <= 0) C = int32_t(std::ceil(target));
+        }
         C = std::max(4, std::min(C, 1 << 20));
     }
 
@@ -185,12 +231,8 @@ spa_status spa_decode_plan(spa_plan* P, int32_t n_req, const spa_req* reqs, int3
     for (const auto& r : ranges) {
         const int32_t pa = r.a / ps, pb = int32_t(cdiv(r.b, ps));
         // at most kMaxSplits splits per range: a request then has <= 2 kMaxSplits partial
-        // records (shared + tail), which the merge combines in one L2 round trip
-        // (small batches, C < cap_min: more splits keep every team streaming; merges are cheap)
-        static const int cap_min = std::getenv("SPA_SPLIT_CAP_MIN") ? std::atoi(std::getenv("SPA_SPLIT_CAP_MIN")) : 0;
-        const int32_t Cr = P->cfg.split_pages > 0 || C < cap_min
-                               ? C
-                               : std::max<int32_t>(C, int32_t(cdiv(pb - pa, kMaxSplits)));
+        // records (shared + tail), which the merge reads in chunks of 16 per L2 round trip
+        const int32_t Cr = P->cfg.split_pages > 0 ? C : std::max<int32_t>(C, int32_t(cdiv(pb - pa, max_splits)));
         for (int32_t s = pa; s < pb; s += Cr) {
             const int32_t e = std::min(pb, s + Cr);
             Desc d{};
@@ -242,8 +284,8 @@ spa_status spa_decode_plan(spa_plan* P, int32_t n_req, const spa_req* reqs, int3
     // this plan uses slot i % kSchedSlots once `owner` == i, so a launch may pop its queue
     // while its predecessors (programmatic dependent launch) still drain; the last team of
     // a launch rewinds the slot and hands it to launch i + kSchedSlots.
-    std::vector<int32_t> sched(size_t(kSchedSlots) * 4, 0);
-    for (int s = 0; s < kSchedSlots; ++s) sched[size_t(s) * 4 + 3] = s;
+    std::vector<int32_t> sched(size_t(kSchedSlots) * kSchedStride, 0);
+    for (int s = 0; s < kSchedSlots; ++s) sched[size_t(s) * kSchedStride + 3] = s;
     P->launches = 0;
 
     // tail-merge tasks (merge_mode 0): every (request with > 1 record, KV head), ordered
@@ -257,9 +299,25 @@ spa_status spa_decode_plan(spa_plan* P, int32_t n_req, const spa_req* reqs, int3
             for (int32_t mi = d.member_off; mi < d.member_off + d.n_members; ++mi)
                 if (members[mi].rec >= 0) last[size_t(members[mi].row) * Hkv + itm.kv_head] = qi;
         }
+        std::vector<int32_t> tasks;
         for (int32_t t = 0; t < int32_t(last.size()); ++t)
-            if (last[t] >= 0) mtask.push_back(t);
-        std::stable_sort(mtask.begin(), mtask.end(), [&](int32_t a, int32_t b) { return last[a] < last[b]; });
+            if (last[t] >= 0) tasks.push_back(t);
+        std::stable_sort(tasks.begin(), tasks.end(), [&](int32_t a, int32_t b) { return last[a] < last[b]; });
+        // subtask codes: task * 64 + 1 + hh (head hh alone: the heads of a task merge in
+        // parallel, ~one L2 round trip after its last record) or, when there are many more
+        // head merges than warps, task * 64 + 0 (one warp merges all G heads of the task with
+        // their loads in flight together: fewer, longer subtasks; needs G x S <= 32)
+        const int64_t warps_total = int64_t(P->num_ctas) * P->teams * P->mt * 2;
+        bool whole = int64_t(tasks.size()) * G > 4 * warps_total;
+        if (const char* e = std::getenv("SPA_MERGE_WHOLE")) whole = std::atoi(e) != 0;   // tests: force a path
+        for (int32_t t : tasks) {
+            const int32_t S = rec_ptr[t / Hkv + 1] - rec_ptr[t / Hkv];
+            if (whole && G <= 8 && G * S <= 32 && S <= 16) {
+                mtask.push_back(t * 64);
+            } else {
+                for (int hh = 0; hh < G; ++hh) mtask.push_back(t * 64 + 1 + hh);
+            }
+        }
     }
 
     // ---- 6. serialise: header + arrays (int32 words)
@@ -274,6 +332,7 @@ spa_status spa_decode_plan(spa_plan* P, int32_t n_req, const spa_req* reqs, int3
     put(H_OFF_DESC, descs.data(), descs.size() * 8);
     put(H_OFF_MEMBER, members.data(), members.size() * 4);
     put(H_OFF_ITEM, items.data(), items.size() * 2);
+    while (H.size() % 32) H.push_back(0);   // 128-B lines: the queue heads are hot atomics
     put(H_OFF_SCHED, sched.data(), sched.size());
     put(H_OFF_QUEUE, order.data(), order.size());
     put(H_OFF_PAGES, pages.data(), pages.size());
@@ -342,6 +401,24 @@ spa_status spa_plan_debug_array(const spa_plan* plan, int32_t which, const int32
     *out_data = H.data() + H[slot];
     *out_len = n * width;
     if (out_row_width) *out_row_width = width;
+    return SPA_OK;
+}
+
+spa_status spa_debug_set_trace(spa_plan* plan, void* buf, int32_t cap) {
+    if (!plan) return fail(SPA_ERR_INVALID_ARG, "null plan");
+    if (buf && cap <= 0) return fail(SPA_ERR_INVALID_ARG, "trace capacity must be > 0");
+    plan->trace = static_cast<unsigned long long*>(buf);
+    plan->trace_cap = buf ? cap : 0;
+    return SPA_OK;
+}
+
+spa_status spa_debug_plan_geometry(const spa_plan* plan, int32_t* out_num_ctas, int32_t* out_teams_per_cta,
+                                   int32_t* out_warps_per_cta) {
+    if (!plan || !out_num_ctas || !out_teams_per_cta || !out_warps_per_cta)
+        return fail(SPA_ERR_INVALID_ARG, "null argument");
+    *out_num_ctas = plan->num_ctas;
+    *out_teams_per_cta = plan->teams;
+    *out_warps_per_cta = plan->teams * plan->mt * 2;   // a team = mt row tiles x 2 key-split warps
     return SPA_OK;
 }
 

@@ -27,15 +27,18 @@ enum MetaHeader : int {
     H_OFF_DESC = 5,
     H_OFF_MEMBER = 6,
     H_OFF_ITEM = 7,
-    H_OFF_SCHED = 8,       // int32[kSchedSlots][4]: queue head, finished teams, tail-merge head, owner launch
+    H_OFF_SCHED = 8,       // int32[kSchedSlots][kSchedStride], 128-B lines: line 0 = {queue head, finished
+                           // CTAs, -, owner launch}; line 1 = {tail-merge queue head}
     H_OFF_QUEUE = 9,       // int32[n_items]: item indices, largest first
     H_OFF_PAGES = 10,
     H_OFF_REC_PTR = 11,
     H_TOTAL = 12,
     H_N_MEMBERS = 13,
     H_N_PAGES = 14,
-    H_OFF_COUNTERS = 15,   // int32 [n_req][Hkv] arrival counters of the fused merge (zero between launches)
-    H_OFF_MTASK = 16,      // int32 [n_mtask]: (row * Hkv + kv_head) merge tasks, earliest-ready first
+    H_OFF_COUNTERS = 15,   // int32 [n_req][Hkv] record arrivals of the in-kernel merges (launch k of a plan
+                           // completes a task at (k + 1) x its records; zeroed by the plan upload)
+    H_OFF_MTASK = 16,      // int32 [n_mtask]: tail-merge subtasks (row * Hkv + kv_head) * 64 + (0: all G
+                           // heads | 1 + head), earliest-ready first
     H_N_MTASK = 17,
     H_WORDS = 20
 };
@@ -64,8 +67,9 @@ constexpr int kPagesPerStage = 2;      // pages of one (KV head) streamed per pi
 constexpr int kWarps = 4;              // warps per CTA of the decode kernel
 constexpr int kSmemBudget = 196 * 1024;
 constexpr int kSchedSlots = 4;         // work-queue counter slots per plan (launch i uses i % 4)
-constexpr int kMaxSplits = 8;          // automatic splits per range (shared region or member tail)
-constexpr int kMergeFast = 16;         // records merged in one round trip (>= 2 kMaxSplits)
+constexpr int kSchedStride = 64;       // int32 words per slot: two 128-B lines
+constexpr int kMaxSplits = 64;         // automatic splits per range (shared region or member tail);
+                                       // 2 kMaxSplits records per request keep the merge on its fast path
 
 // ---------------------------------------------------------------------------- pool
 struct Request {
@@ -118,6 +122,8 @@ struct spa_plan {
     int32_t window = 0;
     int32_t n_req = 0;
     mutable int64_t launches = 0;  // decode launches since the last spa_decode_plan (queue slot owner ids)
+    unsigned long long* trace = nullptr;   // spa_debug_set_trace: timeline buffer (device), or null
+    int32_t trace_cap = 0;
 };
 
 struct spa_comm {

@@ -76,6 +76,8 @@ _SIGS = {
     "spa_plan_debug_array": (c_int32, [c_void_p, c_int32, ctypes.POINTER(P_int32), P_int64, P_int32]),
     "spa_debug_read_bw_ldg": (c_int32, [c_void_p, ctypes.c_size_t, c_void_p, c_void_p]),
     "spa_debug_pool_read_tma": (c_int32, [c_void_p, c_int32, c_int32, c_void_p]),
+    "spa_debug_set_trace": (c_int32, [c_void_p, c_void_p, c_int32]),
+    "spa_debug_plan_geometry": (c_int32, [c_void_p, P_int32, P_int32, P_int32]),
 }
 
 
@@ -330,6 +332,27 @@ class Plan:
         if w.value > 1:
             return [flat[i:i + w.value] for i in range(0, len(flat), w.value)]
         return flat
+
+    def num_ctas_hint(self) -> int:
+        nc, tm, wp = c_int32(), c_int32(), c_int32()
+        _check(lib().spa_debug_plan_geometry(self.h, ctypes.byref(nc), ctypes.byref(tm), ctypes.byref(wp)))
+        return nc.value
+
+    def set_trace(self, cap: int = 0):
+        """Timeline trace of the next decode launches (include/spa_debug.h); cap 0 = off.
+        Returns the (zeroed) uint64 device buffer [num_ctas * warps_per_cta, cap, 2], or None."""
+        import torch  # noqa: WPS433
+
+        if cap <= 0:
+            _check(lib().spa_debug_set_trace(self.h, None, 0))
+            self._trace = None
+            return None
+        nc, tm, wp = c_int32(), c_int32(), c_int32()
+        _check(lib().spa_debug_plan_geometry(self.h, ctypes.byref(nc), ctypes.byref(tm), ctypes.byref(wp)))
+        buf = torch.zeros((nc.value * wp.value, cap, 2), dtype=torch.int64, device=self.pool.k.device)
+        _check(lib().spa_debug_set_trace(self.h, _ptr(buf), cap))
+        self._trace = buf
+        return buf
 
     def decode(self, layer, q, o=None, lse=None, scale=None, stream=None, want_lse=True):
         """q: bf16 [N, Hq, d] (any strides, d contiguous).  Returns (o, lse)."""

@@ -124,6 +124,20 @@ def test_split_merge_equals_unsplit():
     assert torch.equal(o2, o4) and torch.equal(l2, l4)
 
 
+@pytest.mark.parametrize("whole", ["0", "1"])
+def test_tail_merge_group_pass_is_bitwise_per_head(monkeypatch, whole):
+    """The tail merge's one-warp-per-(request, KV head) pass (G x S <= 32) gives the bits of
+    the per-head merges (merge kernel, merge_mode 2)."""
+    monkeypatch.setenv("SPA_MERGE_WHOLE", whole)
+    rec = workloads.random_small(41, workloads.Model("m", 1, 8, 2, 128), max_prefix=120)
+    e0, out0, *_ = run_parity(rec, "peaky", split_pages=3, merge_mode=0)
+    e2, out2, *_ = run_parity(rec, "peaky", split_pages=3, merge_mode=2)
+    _assert_ok(e0)
+    _assert_ok(e2)
+    (o0, l0), (o2, l2) = out0[0], out2[0]
+    assert torch.equal(o0, o2) and torch.equal(l0, l2)
+
+
 @pytest.mark.parametrize("mode", [0, 1, 2])
 @pytest.mark.parametrize("max_rows", [16, 32])
 def test_merge_paths_many_splits(mode, max_rows):
