@@ -1,9 +1,11 @@
 """Build libspa.so in-tree with nvcc for sm_100a (no JIT cache, no torch extension).
 
-    python -m paper_2511_20048_b200.build [--force] [--verbose]
+    python -m paper_2511_20048_b200.build [--force] [--verbose] [--variant NAME --defs "-DX=1 ..."]
 
 Objects go to build/ (git-ignored); the shared library lands next to this file so that
-gpurun snapshots carry it to the GPU box.
+gpurun snapshots carry it to the GPU box.  A variant (performance experiments) builds the
+same sources with extra defines into libspa_NAME.so; SPA_LIB=libspa_NAME.so selects it at
+load time (paper_2511_20048_b200/spa.py).
 """
 from __future__ import annotations
 
@@ -38,8 +40,11 @@ def _nccl_include() -> str:
     raise RuntimeError("nccl.h not found")
 
 
+DEFS: list[str] = []
+
+
 def _flags():
-    return ["-O3", "-std=c++17", "-Xcompiler", "-fPIC,-Wall", "-lineinfo", *ARCH,
+    return ["-O3", "-std=c++17", "-Xcompiler", "-fPIC,-Wall", "-lineinfo", *ARCH, *DEFS,
             "-I", os.path.join(ROOT, "include"), "-I", _nccl_include()]
 
 
@@ -63,7 +68,12 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, variant: str = "", defs: str = "") -> str:
+    global BUILD, OUT, DEFS
+    if variant:
+        BUILD = os.path.join(ROOT, "build", "spa_" + variant)
+        OUT = os.path.join(HERE, f"libspa_{variant}.so")
+        DEFS = defs.split()
     os.makedirs(BUILD, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cpp")) + glob.glob(os.path.join(CSRC, "*.cu")))
     if force:
@@ -83,5 +93,7 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--variant", default="")
+    ap.add_argument("--defs", default="")
     a = ap.parse_args()
-    print(build(a.force, a.verbose))
+    print(build(a.force, a.verbose, a.variant, a.defs))

@@ -48,6 +48,11 @@ struct TeamItem {
     int it, kv_head, n_pages, tok_start, tok_end, member_off, n_members, pad;
 };
 
+#ifndef SPA_QK_CHAINS
+#define SPA_QK_CHAINS 1
+#endif
+constexpr int kQkChains = SPA_QK_CHAINS;   // independent HMMA accumulation chains for QK^T
+
 constexpr int kSmemMax = 232448;   // 227 KB: the sm_100 per-block dynamic shared memory limit
 
 template <int D, int MT, int PPS, int TEAMS_>
@@ -337,6 +342,14 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
                     if (j < npg) {
                         const uint32_t kb = sb + j * 2 * C::PAGE_BYTES;
                         const int key = ((lane >> 4) << 3) + (lane & 7);
+                        // QK^T over the head dimension as kQkChains independent accumulation
+                        // chains per n8 tile (the HMMA dependency chain is the consumer's
+                        // critical path), summed at the end
+                        float sc[kQkChains][2][4];
+#pragma unroll
+                        for (int ch = 0; ch < kQkChains; ++ch)
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) sc[ch][0][e] = sc[ch][1][e] = 0.f;
 #pragma unroll
                         for (int ks = 0; ks < KS; ++ks) {
                             const int dcol = ks * 16 + ((lane >> 3) & 1) * 8;
@@ -344,9 +357,18 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
                                 kb + (dcol >> 6) * 2048 + key * 128 + ((((dcol & 63) >> 3) ^ (key & 7)) << 4);
                             uint32_t b0, b1, b2, b3;
                             ldsm_x4(b0, b1, b2, b3, addr);
-                            mma16816(s[jj][0], qa[ks], b0, b1);
-                            mma16816(s[jj][1], qa[ks], b2, b3);
+                            mma16816(sc[ks % kQkChains][0], qa[ks], b0, b1);
+                            mma16816(sc[ks % kQkChains][1], qa[ks], b2, b3);
                         }
+#pragma unroll
+                        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                float acc_s = sc[0][nt][e];
+#pragma unroll
+                                for (int ch = 1; ch < kQkChains; ++ch) acc_s += sc[ch][nt][e];
+                                s[jj][nt][e] = acc_s;
+                            }
                     }
                 }
                 // mask + scale (log2 domain), row max over this warp's pages

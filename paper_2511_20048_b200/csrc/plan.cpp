@@ -169,6 +169,8 @@ spa_status spa_decode_plan(spa_plan* P, int32_t n_req, const spa_req* reqs, int3
     }
     static const int max_splits =
         std::getenv("SPA_MAX_SPLITS") ? std::max(1, std::atoi(std::getenv("SPA_MAX_SPLITS"))) : kMaxSplits;
+    static const double tail_frac = std::getenv("SPA_TAIL_FRAC") ? std::atof(std::getenv("SPA_TAIL_FRAC")) : 0.0;
+    static const int tail_div = std::getenv("SPA_TAIL_DIV") ? std::max(1, std::atoi(std::getenv("SPA_TAIL_DIV"))) : 8;
     int32_t C = P->cfg.split_pages;
     if (C <= 0) {
         const double target = double(total_pages * Hkv) / double(std::max(1, P->n_teams));
@@ -233,8 +235,25 @@ spa_status spa_decode_plan(spa_plan* P, int32_t n_req, const spa_req* reqs, int3
         // at most kMaxSplits splits per range: a request then has <= 2 kMaxSplits partial
         // records (shared + tail), which the merge reads in chunks of 16 per L2 round trip
         const int32_t Cr = P->cfg.split_pages > 0 ? C : std::max<int32_t>(C, int32_t(cdiv(pb - pa, max_splits)));
-        for (int32_t s = pa; s < pb; s += Cr) {
-            const int32_t e = std::min(pb, s + Cr);
+        // cut points: pieces of Cr pages, except that (automatic splits) the last tail_frac of
+        // a long range is cut into pieces of Cr / tail_div pages.  The largest-first queue
+        // hands those out last, so teams that finish early fill the end of the launch
+        // instead of idling while slower teams finish their big pieces.
+        std::vector<int32_t> cuts{pa};
+        {
+            int32_t main_end = pb;
+            const int32_t small = std::max<int32_t>(4, int32_t(cdiv(Cr, tail_div)));
+            if (P->cfg.split_pages <= 0 && tail_frac > 0 && pb - pa >= 2 * small) {
+                const int32_t tail = std::max<int32_t>(small, int32_t(std::lround((pb - pa) * tail_frac)));
+                main_end = pb - std::min(tail, pb - pa - small);
+            }
+            for (int32_t s = pa + Cr; s < main_end; s += Cr) cuts.push_back(s);
+            if (main_end > cuts.back()) cuts.push_back(main_end);
+            for (int32_t s = main_end + small; s < pb; s += small) cuts.push_back(s);
+            if (cuts.back() != pb) cuts.push_back(pb);
+        }
+        for (size_t ci = 0; ci + 1 < cuts.size(); ++ci) {
+            const int32_t s = cuts[ci], e = cuts[ci + 1];
             Desc d{};
             d.page_off = int32_t(pages.size());
             d.n_pages = e - s;

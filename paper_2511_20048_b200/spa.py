@@ -14,7 +14,9 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libspa.so")
+# SPA_LIB: a variant build (libspa_NAME.so next to this file, build.py --variant) for
+# performance experiments; the default is the library build() produces
+LIB_PATH = os.path.join(HERE, os.path.basename(os.environ.get("SPA_LIB", "libspa.so")))
 
 SPA_OK, SPA_ERR_INVALID_ARG, SPA_ERR_NO_PAGES, SPA_ERR_BAD_REQUEST = 0, 1, 2, 3
 SPA_ERR_CUDA, SPA_ERR_NCCL, SPA_ERR_UNSUPPORTED, SPA_ERR_NO_DEVICE = 4, 5, 6, 7
