@@ -8,8 +8,9 @@ seeded input generators in `spa_inputs`, which hold none of the method's arithme
 
 Contents
   attention.py  decode attention, written as its plain definition (softmax(scale q K^T) V
-                per query head, GQA head mapping, optional sliding window), and the
-                split-KV log-sum-exp merge.
+                per query head, GQA head mapping, optional sliding window), the causal
+                extend (prefill of a request's last T tokens) as that definition per
+                token, and the split-KV log-sum-exp merge.
   kvmodel.py    a dense logical KV model (a fork is a physical copy) plus an independent
                 model of the documented paging policy (lowest-free page id, refcounts,
                 copy-on-write of the partial last page).

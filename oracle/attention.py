@@ -14,6 +14,9 @@ token against every key of its context, which for a grouped-query model reads:
     LSE_h = m + ln sum_j exp(z_j - m),  m = max_j z_j           (reading #7: natural log)
     O[h]  = sum_j exp(z_j - LSE_h) * V[j, g(h), :]
 
+The extend step (F2) is the same definition per query token t of a request's last T
+tokens: the context is cut after the token's own position (causal).
+
 The split-KV merge (north_star "split-KV partial-LSE merge"): for partials (O_s, LSE_s)
 computed over disjoint key subsets,
 
@@ -57,6 +60,32 @@ def decode_attention(q: np.ndarray, K: np.ndarray, V: np.ndarray, scale: float, 
         P = np.exp(Z - lse)
         O[g * G:(g + 1) * G] = P @ Vg
         LSE[g * G:(g + 1) * G] = lse[:, 0]
+    return O, LSE
+
+
+def extend_attention(Q: np.ndarray, K: np.ndarray, V: np.ndarray, scale: float, window: int = 0):
+    """The last T tokens of one request as queries: the prefill of an extension (the
+    speculative prompt appended to a fork of c_i, "prefill overhead is added
+    once per speculative request"), causal.
+
+    Q: [T, Hq, d] fp64 queries of the request's last T tokens, in order.
+    K, V: [n, Hkv, d] fp64 logical keys/values of the request, n >= T, the T new tokens
+          included (appended before attention, reading #8).
+    Token t sits at position p = n - T + t and attends to keys [max(0, p + 1 - W), p + 1)
+    (window W > 0, reading #9) or [0, p + 1): that is, by definition, the decode attention
+    of the request's context cut after position p -- which is what is computed here.
+    Returns (O [T, Hq, d] fp64, LSE [T, Hq] fp64).
+    """
+    Q = np.asarray(Q, dtype=np.float64)
+    T = Q.shape[0]
+    n = K.shape[0]
+    if T < 1 or T > n:
+        raise ValueError("need 1 <= T <= n query tokens")
+    O = np.zeros(Q.shape)
+    LSE = np.zeros(Q.shape[:2])
+    for t in range(T):
+        p = n - T + t
+        O[t], LSE[t] = decode_attention(Q[t], K[:p + 1], V[:p + 1], scale, window)
     return O, LSE
 
 

@@ -9,7 +9,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .attention import decode_attention
+from .attention import decode_attention, extend_attention
 from .kvmodel import OK, LogicalKV, PagingModel
 
 
@@ -68,4 +68,22 @@ class Replay:
             K = bits_to_f64(self.kv.K[nm][layer_pos])
             V = bits_to_f64(self.kv.V[nm][layer_pos])
             O[i], LSE[i] = decode_attention(bits_to_f64(q_bits[i]), K, V, scale, window)
+        return O, LSE
+
+    def expected_extend(self, layer_pos: int, q_rows_bits, n_query, names=None, window: int = 0, scale=None):
+        """fp64 (O [rows, Hq, d], LSE [rows, Hq]) of an extend batch: request i's last
+        n_query[i] tokens are rows (request-major, token-minor), as spa_extend_plan numbers them."""
+        m = self.inputs.recipe.model
+        scale = m.softmax_scale if scale is None else scale
+        names = self.inputs.batch if names is None else names
+        rows = int(sum(n_query))
+        O = np.zeros((rows, m.num_q_heads, m.head_dim))
+        LSE = np.zeros((rows, m.num_q_heads))
+        r0 = 0
+        for i, nm in enumerate(names):
+            T = int(n_query[i])
+            K = bits_to_f64(self.kv.K[nm][layer_pos])
+            V = bits_to_f64(self.kv.V[nm][layer_pos])
+            O[r0:r0 + T], LSE[r0:r0 + T] = extend_attention(bits_to_f64(q_rows_bits[r0:r0 + T]), K, V, scale, window)
+            r0 += T
         return O, LSE
