@@ -124,8 +124,8 @@ spa_status spa_pool_free_pages(const spa_pool* pool, int32_t* out_pages, int32_t
  * --------------------------------------------------------------------------------- */
 typedef struct spa_plan_config {
     int32_t sharing;        /* 1: group by shared prefix (default); 0: every request alone (control) */
-    int32_t max_rows;       /* 16 or 32: query rows (members x G) per work item; larger groups
-                               are cut into sub-groups.  0 = 16                                 */
+    int32_t max_rows;       /* 16, 32 or 64: query rows (rows x G) per work item; larger groups
+                               are cut into sub-groups.  0 = 16 (64: extend batches, one team)  */
     int32_t split_pages;    /* max pages per split; 0 = auto (balance over the persistent grid)  */
     int32_t num_ctas;       /* persistent grid size; 0 = number of SMs                            */
     int32_t merge_mode;     /* where split partials are merged (spa_merge_splits semantics always):
@@ -151,8 +151,20 @@ spa_status spa_plan_destroy(spa_plan* plan);
  *   graphs captured over this plan). */
 spa_status spa_decode_plan(spa_plan* plan, int32_t n_req, const spa_req* reqs, int32_t window, void* stream);
 
+/* (Re)plan an EXTEND batch (the prefill of a speculative prompt
+ * over its shared context): request i contributes n_query[i] >= 1 query
+ * rows, its LAST n_query[i] tokens (already appended), so row token t < n_query[i] sits at
+ * position p = n_i - n_query[i] + t and attends causally to keys [max(0, p + 1 - window),
+ * p + 1) (window <= 0: [0, p + 1)).  Rows are numbered request-major, token-minor (the
+ * packing of spa_kv_append's k_new/v_new); q/o/lse of spa_decode_attention are indexed by
+ * this row number.  n_query = NULL means 1 for every request: spa_decode_plan.  Rows of
+ * the requests sharing a prefix are one group (the shared pages are read once per KV head
+ * and sub-group of max_rows / G rows); a request's own rows share its tail range. */
+spa_status spa_extend_plan(spa_plan* plan, int32_t n_req, const spa_req* reqs, const int32_t* n_query,
+                           int32_t window, void* stream);
+
 typedef struct spa_plan_stats {
-    int32_t n_req, n_groups, n_desc, n_items, n_records, n_teams, rows_max, generation;
+    int32_t n_req /* query rows */, n_groups, n_desc, n_items, n_records, n_teams, rows_max, generation;
     int64_t unique_tokens;    /* sum over work descriptors of key tokens read, per KV head     */
     int64_t unshared_tokens;  /* sum over requests of attended keys, per KV head (no sharing)  */
     int64_t pages_read;       /* pages read per KV head (page-granular, incl. partial pages)   */

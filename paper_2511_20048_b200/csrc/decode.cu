@@ -282,8 +282,9 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
         const bool active = wt * 16 < R;   // identical for the KW warps of a row tile
         const int row0 = wt * 16 + (lane >> 2), row1 = row0 + 8;
 
-        // ---- per-row setup: member, window bound, query fragments (padding rows: q = 0, lo = 0)
-        int lo0 = 0, lo1 = 0;
+        // ---- per-row setup: member, window bound lo and causal bound hi (keys [lo, hi) are
+        //      live), query fragments (padding rows: q = 0, lo = 0, hi = INT_MAX)
+        int lo0 = 0, lo1 = 0, hi0 = INT_MAX, hi1 = INT_MAX;
         uint32_t qa[KS][4];
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) qa[ks][0] = qa[ks][1] = qa[ks][2] = qa[ks][3] = 0u;
@@ -294,12 +295,14 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
                 const int mb = row0 / G;
                 const Member m = mems[dsc.member_off + mb];
                 lo0 = m.lo;
+                hi0 = m.hi;
                 q0 = p.q + m.row * p.q_sr + (itm.kv_head * G + row0 - mb * G) * p.q_sh;
             }
             if (row1 < R) {
                 const int mb = row1 / G;
                 const Member m = mems[dsc.member_off + mb];
                 lo1 = m.lo;
+                hi1 = m.hi;
                 q1 = p.q + m.row * p.q_sr + (itm.kv_head * G + row1 - mb * G) * p.q_sh;
             }
             const int cq = 2 * (lane & 3);
@@ -315,10 +318,14 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
                 }
             }
         }
-        // keys >= lo_warp are inside every row's window: such pages need no window mask
-        int lo_warp = max(lo0, lo1);
+        // keys in [lo_warp, hi_warp) are live for every row of the warp: such pages need no mask
+        int lo_warp = max(lo0, lo1), hi_warp = min(hi0, hi1);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) lo_warp = max(lo_warp, __shfl_xor_sync(0xffffffffu, lo_warp, o));
+        for (int o = 16; o > 0; o >>= 1) {
+            lo_warp = max(lo_warp, __shfl_xor_sync(0xffffffffu, lo_warp, o));
+            hi_warp = min(hi_warp, __shfl_xor_sync(0xffffffffu, hi_warp, o));
+        }
+        hi_warp = min(hi_warp, dsc.tok_end);
         // running max per row, log2 units, raised lazily (only when a page's max exceeds it
         // by > kRescale, so P <= 2^kRescale); the same m is used for P, l and the LSE.
         constexpr float kRescale = 8.f;
@@ -377,7 +384,7 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
                 for (int jj = 0; jj < JW; ++jj) {
                     const int j = wk + jj * KW;
                     const int tokp = dsc.tok_start + (st * PPS + j) * kPageSize;
-                    const bool unmasked = (j < npg) && (tokp >= lo_warp) && (tokp + kPageSize <= dsc.tok_end);
+                    const bool unmasked = (j < npg) && (tokp >= lo_warp) && (tokp + kPageSize <= hi_warp);
                     if (unmasked) {
 #pragma unroll
                         for (int nt = 0; nt < 2; ++nt)
@@ -395,7 +402,8 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
                             for (int e = 0; e < 4; ++e) {
                                 const int tok = tokp + nt * 8 + 2 * (lane & 3) + (e & 1);
                                 const int lo = (e < 2) ? lo0 : lo1;
-                                const bool ok = (j < npg) && (tok < dsc.tok_end) && (tok >= lo);
+                                const int hi = (e < 2) ? hi0 : hi1;
+                                const bool ok = (j < npg) && (tok < dsc.tok_end) && (tok >= lo) && (tok < hi);
                                 const float v = ok ? s[jj][nt][e] * p.scale_log2 : -INFINITY;
                                 s[jj][nt][e] = v;
                                 if (e < 2) mx0 = fmaxf(mx0, v);
@@ -676,11 +684,15 @@ static int launch_decode_d(const spa_plan* P, const DecodeParams& dp, void* stre
         if (P->teams == 2) return launch_decode_t<D, 1, 2, 2>(P, dp, stream);
         return launch_decode_t<D, 1, 2, 4>(P, dp, stream);
     }
+    if (P->mt == 4) return launch_decode_t<D, 4, 2, 1>(P, dp, stream);
     if (P->teams == 1) return launch_decode_t<D, 2, 2, 1>(P, dp, stream);
     return launch_decode_t<D, 2, 2, 2>(P, dp, stream);
 }
 
-bool decode_teams_supported(int mt, int teams) { return teams == 1 || teams == 2 || (teams == 4 && mt == 1); }
+bool decode_teams_supported(int mt, int teams) {
+    if (mt == 4) return teams == 1;
+    return teams == 1 || teams == 2 || (teams == 4 && mt == 1);
+}
 
 int launch_decode(const spa_plan* P, int32_t layer, const void* q, int64_t q_sr, int64_t q_sh, void* o, int64_t o_sr,
                   int64_t o_sh, float* lse, int64_t l_sr, int64_t l_sh, float scale, void* stream) {

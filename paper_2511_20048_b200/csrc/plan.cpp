@@ -55,7 +55,8 @@ spa_status spa_plan_create(spa_pool* pool, const spa_plan_config* cfg, spa_plan*
     c.sharing = 1;
     if (cfg) c = *cfg;
     if (c.max_rows == 0) c.max_rows = 16;
-    if (c.max_rows != 16 && c.max_rows != 32) return fail(SPA_ERR_UNSUPPORTED, "max_rows must be 16 or 32");
+    if (c.max_rows != 16 && c.max_rows != 32 && c.max_rows != 64)
+        return fail(SPA_ERR_UNSUPPORTED, "max_rows must be 16, 32 or 64");
     if (c.split_pages < 0 || c.num_ctas < 0) return fail(SPA_ERR_INVALID_ARG, "negative plan option");
     if (c.merge_mode < 0 || c.merge_mode > 2) return fail(SPA_ERR_INVALID_ARG, "merge_mode must be 0, 1 or 2");
     const int G = pool->cfg.num_q_heads / pool->cfg.num_kv_heads;
@@ -69,10 +70,10 @@ spa_status spa_plan_create(spa_pool* pool, const spa_plan_config* cfg, spa_plan*
     P->num_ctas = ctas;
     int teams = c.teams_per_cta;
     if (const char* e = std::getenv("SPA_TEAMS")) teams = std::atoi(e);
-    if (teams == 0) teams = P->mt == 1 ? 4 : 2;
+    if (teams == 0) teams = P->mt == 1 ? 4 : P->mt == 2 ? 2 : 1;
     if (!decode_teams_supported(P->mt, teams)) {
         delete P;
-        return fail(SPA_ERR_UNSUPPORTED, "teams_per_cta must be 1, 2 or 4 (4 only with max_rows 16)");
+        return fail(SPA_ERR_UNSUPPORTED, "teams_per_cta must be 1, 2 or 4 (4 only with max_rows 16, 1 with 64)");
     }
     P->teams = teams;
     P->n_teams = ctas * teams;
@@ -87,76 +88,129 @@ spa_status spa_plan_destroy(spa_plan* plan) {
     return SPA_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// One query row of the batch: a token of a request that attends to keys [lo, hi) of the
+// request's KV (hi = its causal length, position + 1); `first_new` = the request's first
+// token appended in this step (descriptors holding keys >= first_new are produced right
+// before attention: the kernel does not prefetch them ahead of its dependency wait).
+struct VRow {
+    const Request* req;
+    int32_t hi, first_new;
+};
+
+spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, void* stream);
+
+}  // namespace
+
+extern "C" {
+
 spa_status spa_decode_plan(spa_plan* P, int32_t n_req, const spa_req* reqs, int32_t window, void* stream) {
+    return spa_extend_plan(P, n_req, reqs, nullptr, window, stream);
+}
+
+spa_status spa_extend_plan(spa_plan* P, int32_t n_req, const spa_req* reqs, const int32_t* n_query, int32_t window,
+                           void* stream) {
     if (!P) return fail(SPA_ERR_INVALID_ARG, "null plan");
     spa_pool* pool = P->pool;
     if (n_req < 0 || (n_req > 0 && !reqs)) return fail(SPA_ERR_INVALID_ARG, "bad request list");
+    std::vector<VRow> V;
+    V.reserve(size_t(n_req));
+    std::unordered_set<int64_t> seen;
+    for (int i = 0; i < n_req; ++i)
+        if (!seen.insert(reqs[i]).second) return fail(SPA_ERR_INVALID_ARG, "plan: request listed twice");
+    for (int i = 0; i < n_req; ++i) {
+        auto it = pool->reqs.find(reqs[i]);
+        if (it == pool->reqs.end()) return fail(SPA_ERR_BAD_REQUEST, "plan: unknown request " + std::to_string(reqs[i]));
+        const Request* r = &it->second;
+        if (r->len <= 0) return fail(SPA_ERR_INVALID_ARG, "plan: decode over an empty request (reading #11)");
+        const int32_t nq = n_query ? n_query[i] : 1;
+        if (nq < 1 || nq > r->len) return fail(SPA_ERR_INVALID_ARG, "plan: n_query must be in [1, request length]");
+        for (int32_t t = 0; t < nq; ++t) V.push_back(VRow{r, r->len - nq + t + 1, r->len - nq});
+    }
+    if (V.size() > size_t(1) << 30) return fail(SPA_ERR_INVALID_ARG, "plan: too many query rows");
+    return plan_rows(P, V, window, stream);
+}
+
+}  // extern "C"
+
+namespace {
+
+spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, void* stream) {
+    spa_pool* pool = P->pool;
     const int ps = pool->cfg.page_size;
     const int Hkv = pool->cfg.num_kv_heads;
     const int G = pool->cfg.num_q_heads / Hkv;
-    std::vector<const Request*> R(n_req);
-    {
-        std::unordered_set<int64_t> seen;
-        for (int i = 0; i < n_req; ++i)
-            if (!seen.insert(reqs[i]).second) return fail(SPA_ERR_INVALID_ARG, "plan: request listed twice");
-        for (int i = 0; i < n_req; ++i) {
-            auto it = pool->reqs.find(reqs[i]);
-            if (it == pool->reqs.end()) return fail(SPA_ERR_BAD_REQUEST, "plan: unknown request " + std::to_string(reqs[i]));
-            if (it->second.len <= 0) return fail(SPA_ERR_INVALID_ARG, "plan: decode over an empty request (reading #11)");
-            R[i] = &it->second;
-        }
-    }
+    const int n_req = int(V.size());   // query rows
+    // window (reading #9): a query at position p attends to keys [p + 1 - W, p]
     std::vector<int32_t> lo(n_req);
-    for (int i = 0; i < n_req; ++i) lo[i] = window > 0 ? std::max<int32_t>(0, R[i]->len - window) : 0;
+    for (int i = 0; i < n_req; ++i) lo[i] = window > 0 ? std::max<int32_t>(0, V[i].hi - window) : 0;
 
-    // ---- 1. groups (first page id), then sub-groups of at most max_rows / G members
+    // ---- 1. groups (first page id; sharing off: each request alone), then sub-groups of at
+    //      most max_rows / G rows (the rows of a request stay consecutive)
     std::vector<std::vector<int>> groups;
-    if (P->cfg.sharing) {
-        std::unordered_map<int32_t, int> by_root;
+    {
+        std::unordered_map<int64_t, int> by_key;
         for (int i = 0; i < n_req; ++i) {
-            auto ins = by_root.emplace(R[i]->pages[0], int(groups.size()));
+            const int64_t key = P->cfg.sharing ? int64_t(V[i].req->pages[0]) : int64_t(reinterpret_cast<intptr_t>(V[i].req));
+            auto ins = by_key.emplace(key, int(groups.size()));
             if (ins.second) groups.emplace_back();
             groups[ins.first->second].push_back(i);
         }
-    } else {
-        for (int i = 0; i < n_req; ++i) groups.push_back({i});
     }
     const int max_members = std::max(1, P->cfg.max_rows / G);
 
-    // ---- 2. ranges
+    // ---- 2. ranges: the sub-group's common page-id prefix [., S) holds all its rows; each
+    //      request's rows share one tail range [., max hi) (per-row lo / hi are masks)
     std::vector<Range> ranges;
     int n_groups = 0;
     int64_t unique_tokens = 0, unshared_tokens = 0;
-    for (int i = 0; i < n_req; ++i) unshared_tokens += R[i]->len - lo[i];
+    for (int i = 0; i < n_req; ++i) unshared_tokens += V[i].hi - lo[i];
     for (const auto& grp : groups) {
         for (size_t s0 = 0; s0 < grp.size(); s0 += max_members) {
             std::vector<int> sg(grp.begin() + s0, grp.begin() + std::min(grp.size(), s0 + max_members));
             const int gid = n_groups++;
             int32_t cp = 0;
-            if (sg.size() > 1) {
-                const auto& t0 = R[sg[0]]->pages;
+            bool one_table = true;
+            for (int m : sg) one_table &= V[m].req == V[sg[0]].req;
+            if (sg.size() > 1 && !one_table) {
+                const auto& t0 = V[sg[0]].req->pages;
                 for (;; ++cp) {
                     bool ok = true;
                     for (int m : sg) {
-                        const auto& t = R[m]->pages;
-                        if (int64_t(R[m]->len) < int64_t(cp + 1) * ps || t[cp] != t0[cp]) { ok = false; break; }
+                        const auto& t = V[m].req->pages;
+                        if (int64_t(V[m].hi) < int64_t(cp + 1) * ps || t[cp] != t0[cp]) { ok = false; break; }
                     }
                     if (!ok) break;
                 }
             }
             const int32_t S = cp * ps;
-            if (S == 0) {
-                for (int m : sg) ranges.push_back(Range{0, gid, {m}, lo[m], R[m]->len, &R[m]->pages});
-                continue;
+            if (S > 0) {
+                std::vector<int> shared;
+                int32_t lo_min = S;
+                for (int m : sg)
+                    if (lo[m] < S) { shared.push_back(m); lo_min = std::min(lo_min, lo[m]); }
+                if (!shared.empty()) ranges.push_back(Range{0, gid, shared, lo_min, S, &V[sg[0]].req->pages});
             }
-            std::vector<int> shared;
-            int32_t lo_min = S;
-            for (int m : sg)
-                if (lo[m] < S) { shared.push_back(m); lo_min = std::min(lo_min, lo[m]); }
-            if (!shared.empty()) ranges.push_back(Range{0, gid, shared, lo_min, S, &R[sg[0]]->pages});
-            for (int m : sg) {
-                const int32_t a = std::max(S, lo[m]);
-                if (a < R[m]->len) ranges.push_back(Range{1, gid, {m}, a, R[m]->len, &R[m]->pages});
+            // per request (page table): its rows' keys beyond S
+            for (size_t k = 0; k < sg.size();) {
+                size_t e = k;
+                while (e < sg.size() && V[sg[e]].req == V[sg[k]].req) ++e;
+                std::vector<int> mem;
+                int32_t a = INT32_MAX, b = 0;
+                for (size_t x = k; x < e; ++x) {
+                    const int m = sg[x];
+                    const int32_t am = std::max(S, lo[m]);
+                    if (am < V[m].hi) {
+                        mem.push_back(m);
+                        a = std::min(a, am);
+                        b = std::max(b, V[m].hi);
+                    }
+                }
+                if (!mem.empty()) ranges.push_back(Range{S > 0 ? 1 : 0, gid, mem, a, b, &V[sg[k]].req->pages});
+                k = e;
             }
         }
     }
@@ -266,11 +320,11 @@ spa_status spa_decode_plan(spa_plan* P, int32_t n_req, const spa_req* reqs, int3
             // key/value is produced right before attention, so the kernel does not prefetch
             // it ahead of its programmatic-dependency wait
             for (int m : r.members)
-                if (d.tok_end >= R[m]->len) d.kind |= 4;
+                if (d.tok_end > V[m].first_new) d.kind |= 4;
             d.group = r.group;
             for (int32_t p = s; p < e; ++p) pages.push_back((*r.table)[p]);
             for (int m : r.members) {
-                members.push_back(Member{m, lo[m], 0, 0});
+                members.push_back(Member{m, lo[m], 0, V[m].hi});
                 occ[m] += 1;
             }
             descs.push_back(d);
@@ -394,6 +448,10 @@ spa_status spa_decode_plan(spa_plan* P, int32_t n_req, const spa_req* reqs, int3
     st.generation = P->generation;
     return SPA_OK;
 }
+
+}  // namespace
+
+extern "C" {
 
 spa_status spa_plan_get_stats(const spa_plan* plan, spa_plan_stats* out) {
     if (!plan || !out) return fail(SPA_ERR_INVALID_ARG, "null argument");

@@ -55,7 +55,7 @@ struct Member {
     int32_t row;   // batch row (index into q / o / lse)
     int32_t lo;    // window lower bound: keys j < lo are masked for this member
     int32_t rec;   // partial record index, or -1: write final O / LSE directly
-    int32_t pad;
+    int32_t hi;    // causal bound: keys j >= hi are masked for this row (decode: the length)
 };
 
 struct Item {

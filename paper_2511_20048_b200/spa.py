@@ -63,6 +63,7 @@ _SIGS = {
     "spa_plan_create": (c_int32, [c_void_p, ctypes.POINTER(spa_plan_config), ctypes.POINTER(c_void_p)]),
     "spa_plan_destroy": (c_int32, [c_void_p]),
     "spa_decode_plan": (c_int32, [c_void_p, c_int32, P_int64, c_int32, c_void_p]),
+    "spa_extend_plan": (c_int32, [c_void_p, c_int32, P_int64, P_int32, c_int32, c_void_p]),
     "spa_plan_get_stats": (c_int32, [c_void_p, ctypes.POINTER(spa_plan_stats)]),
     "spa_decode_attention": (c_int32, [c_void_p, c_int32, c_void_p, c_int64, c_int64, c_void_p, c_int64, c_int64,
                                        c_void_p, c_int64, c_int64, c_float, c_void_p]),
@@ -310,14 +311,25 @@ class Plan:
         except Exception:  # noqa: BLE001
             pass
 
-    def plan(self, reqs, window=0, stream=None, check=True):
+    def plan(self, reqs, window=0, stream=None, check=True, n_query=None):
+        """Plan a decode batch (one query row per request), or with n_query (one int per
+        request) an extend batch: request i's last n_query[i] tokens are query rows
+        (request-major, token-minor), each attending causally (include/spa.h)."""
         n = len(reqs)
         ra = (c_int64 * max(n, 1))(*reqs)
-        st = lib().spa_decode_plan(self.h, n, ra, int(window),
-                                   _stream_ptr(stream) if self.pool.k is not None else None)
+        sp = _stream_ptr(stream) if self.pool.k is not None else None
+        if n_query is None:
+            st = lib().spa_decode_plan(self.h, n, ra, int(window), sp)
+            rows = n
+        else:
+            if len(n_query) != n:
+                raise ValueError("n_query needs one entry per request")
+            qa = (c_int32 * max(n, 1))(*[int(x) for x in n_query])
+            st = lib().spa_extend_plan(self.h, n, ra, qa, int(window), sp)
+            rows = int(sum(int(x) for x in n_query))
         if check:
             _check(st)
-            self.n_req = n
+            self.n_req = rows
         return st
 
     def stats(self) -> dict:

@@ -34,7 +34,9 @@ def build(recipe, num_pages=None):
     return pool, [ids[n] for n in batch]
 
 
-def check_plan(pool, plan, reqs, window):
+def check_plan(pool, plan, reqs, window, n_query=None):
+    """Every query row's live keys [lo, hi) are covered exactly once, through the right
+    physical pages; rows are request-major, token-minor (spa_extend_plan)."""
     descs = plan.debug_array(DBG_DESC)
     mems = plan.debug_array(DBG_MEMBER)
     items = plan.debug_array(DBG_ITEM)
@@ -42,8 +44,15 @@ def check_plan(pool, plan, reqs, window):
     pages = plan.debug_array(DBG_PAGES)
     rec_ptr = plan.debug_array(DBG_REC_PTR)
     Hkv = pool.cfg.num_kv_heads
-    N = len(reqs)
-    tables = [pool.page_table(r) for r in reqs]
+    n_query = [1] * len(reqs) if n_query is None else list(n_query)
+    row_tab, row_hi = [], []
+    for r, nq in zip(reqs, n_query):
+        _, tab, n = pool.page_table(r)
+        for t in range(nq):
+            row_tab.append(tab)
+            row_hi.append(n - nq + t + 1)
+    N = len(row_tab)
+    row_lo = [max(0, h - window) if window > 0 else 0 for h in row_hi]
     cover = [dict() for _ in range(N)]   # token -> count
     occ = [0] * N
     recs = [[] for _ in range(N)]
@@ -51,18 +60,16 @@ def check_plan(pool, plan, reqs, window):
         page_off, n_pages, t0, t1, moff, nmem, kind, group = d
         assert t0 % 16 == 0 and t1 <= t0 + 16 * n_pages and t1 > t0 + 16 * (n_pages - 1)
         for mi in range(moff, moff + nmem):
-            row, lo, rec, _ = mems[mi]
+            row, lo, rec, hi = mems[mi]
             occ[row] += 1
             recs[row].append(rec)
-            _, tab, n = tables[row]
-            assert lo == (max(0, n - window) if window > 0 else 0)
-            for t in range(max(t0, lo), t1):
+            tab = row_tab[row]
+            assert lo == row_lo[row] and hi == row_hi[row]
+            for t in range(max(t0, lo), min(t1, hi)):
                 assert pages[page_off + (t - t0) // 16] == tab[t // 16], "wrong physical page"
                 cover[row][t] = cover[row][t] + 1 if t in cover[row] else 1
     for r in range(N):
-        _, tab, n = tables[r]
-        lo = max(0, n - window) if window > 0 else 0
-        assert sorted(cover[r]) == list(range(lo, n)), r
+        assert sorted(cover[r]) == list(range(row_lo[r], row_hi[r])), r
         assert all(c == 1 for c in cover[r].values())
         if occ[r] == 1:
             assert recs[r] == [-1] and rec_ptr[r + 1] == rec_ptr[r]
@@ -176,3 +183,52 @@ def test_lpt_schedule_is_balanced():
         heapq.heappush(teams, (load + descs[items[i][0]][1] + 1, t))
     loads = [l for l, _ in teams]
     assert max(loads) <= 1.15 * np.mean(loads)
+
+
+@settings(max_examples=60, deadline=None)
+@given(st.integers(0, 100_000), st.sampled_from([0, 0, 5, 16, 40]), st.booleans(),
+       st.sampled_from([16, 32, 64]), st.sampled_from([0, 1, 3]))
+def test_extend_batches_cover_every_key_once(seed, window, sharing, max_rows, split):
+    """F2: requests contribute their last n_query tokens as causal query rows."""
+    rec = workloads.random_small(seed)
+    pool, reqs = build(rec)
+    G = rec.model.num_q_heads // rec.model.num_kv_heads
+    if G > max_rows:
+        return
+    rng = np.random.default_rng(seed)
+    n_query = [int(rng.integers(1, min(pool.page_table(r)[2], 40) + 1)) for r in reqs]
+    plan = spa.Plan(pool, sharing=sharing, max_rows=max_rows, split_pages=split, num_ctas=3)
+    plan.plan(reqs, window, n_query=n_query)
+    check_plan(pool, plan, reqs, window, n_query)
+    assert plan.stats()["n_req"] == sum(n_query)
+
+
+def test_extend_rows_share_the_prefix():
+    """A fork's speculative prompt (16 query tokens) and its parent's decode token: the
+    parent/fork common prefix is read once per KV head and sub-group of max_rows rows."""
+    rec = workloads.qwen(seed=1, n_agents=4)
+    pool, reqs = build(rec)
+    n_query = [1 if i % 2 == 0 else 16 for i in range(len(reqs))]   # batch = parent, fork, ...
+    p64 = spa.Plan(pool, max_rows=64, num_ctas=8)
+    p64.plan(reqs, 0, n_query=n_query)
+    check_plan(pool, p64, reqs, 0, n_query)
+    p16 = spa.Plan(pool, max_rows=16, num_ctas=8)
+    p16.plan(reqs, 0, n_query=n_query)
+    check_plan(pool, p16, reqs, 0, n_query)
+    # 17 rows x G=5 = 85 rows: 2 sub-groups at 64 rows, 6 at 16 -> shared prefix read 2 vs 6 times
+    shared = sum(g.prefix // 16 * 16 for g in rec.groups)
+    assert p64.stats()["unique_tokens"] < p16.stats()["unique_tokens"]
+    assert p64.stats()["unique_tokens"] >= 2 * shared
+
+
+def test_extend_plan_errors():
+    pool = spa.Pool(1, 4, 2, 64, 8)
+    a = pool.alloc()
+    pool.append([a], [5])
+    plan = spa.Plan(pool)
+    for bad in ([0], [6], [-1]):
+        with pytest.raises(SpaError) as e:
+            plan.plan([a], n_query=bad)
+        assert e.value.status == spa.SPA_ERR_INVALID_ARG
+    plan.plan([a], n_query=[5])
+    assert plan.stats()["n_req"] == 5
