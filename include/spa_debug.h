@@ -64,6 +64,12 @@ spa_status spa_debug_set_trace(spa_plan* plan, void* buf, int32_t cap);
 spa_status spa_debug_plan_geometry(const spa_plan* plan, int32_t* out_num_ctas, int32_t* out_teams_per_cta,
                                    int32_t* out_warps_per_cta);
 
+/* tcgen05 self-test (one CTA): q [128][128], k [32][128], v [32][128] bf16 row-major (device);
+ * out_s [128][32] = q k^T (fp32), out_o [128][128] = bf16(out_s) v (fp32).  Exercises the
+ * shared-memory / instruction descriptors and tensor-memory layouts of the extend kernel. */
+spa_status spa_debug_umma_selftest(const void* q, const void* k, const void* v, float* out_s, float* out_o,
+                                   void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -13,6 +13,7 @@
 
 #include "device_util.cuh"
 #include "spa_internal.h"
+#include "umma.cuh"
 #include "../../include/spa_debug.h"
 
 namespace spa {
@@ -144,6 +145,95 @@ static cudaError_t launch_probe(const spa_pool* pool, const CUtensorMap& mk, con
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- tcgen05 self-test
+// One CTA: S = Q K^T (M=128, N=16 per page, K=128 in 8 steps) from 128-B-swizzled shared
+// memory into tensor memory, P = bf16(S) stored back to tensor memory, O = P V (A from
+// tensor memory, V as an MN-major operand, one K=16 MMA per page).  Checks the descriptor
+// and tensor-memory conventions the extend kernel relies on against a host reference.
+__global__ void __launch_bounds__(192, 1)
+    umma_selftest_kernel(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v, float* out_s,
+                         float* out_o) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t QB = sbase, KB = sbase + 32768, VB = KB + 8192, BAR = VB + 8192, TSLOT = BAR + 64;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // stage operands: Q [128][128] -> two 16-KB column chunks; K, V [32][128] -> 2 pages of
+    // [chunk][16 rows][128 B], exactly as the TMA boxes of the pool land
+    for (int i = tid; i < 128 * 16; i += blockDim.x) {
+        const int r = i >> 4, u = i & 15;   // 16-B unit u of row r (8 bf16)
+        const uint4 val = reinterpret_cast<const uint4*>(q + r * 128)[u];
+        *reinterpret_cast<uint4*>(smem + (u >> 3) * 16384 + umma::sw128_offset(r, u & 7)) = val;
+    }
+    for (int i = tid; i < 32 * 16; i += blockDim.x) {
+        const int r = i >> 4, u = i & 15, pg = r >> 4, rr = r & 15;
+        const uint32_t off = pg * 4096 + (u >> 3) * 2048 + umma::sw128_offset(rr, u & 7);
+        *reinterpret_cast<uint4*>(smem + 32768 + off) = reinterpret_cast<const uint4*>(k + r * 128)[u];
+        *reinterpret_cast<uint4*>(smem + 32768 + 8192 + off) = reinterpret_cast<const uint4*>(v + r * 128)[u];
+    }
+    if (tid == 0) {
+        for (int b = 0; b < 3; ++b) mbar_init(BAR + b * 8, b == 1 ? 128 : 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    umma::fence_proxy_async_smem();
+    __syncthreads();
+    if (warp == 0) umma::tmem_alloc(TSLOT, 256);
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+    const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + (TSLOT - sbase));
+    const uint32_t S_COL = 0, P_COL = 32, O_COL = 128;
+    if (tid == 32) {
+        const uint32_t id_s = umma::idesc_bf16_f32(128, 16, false, false);
+        for (int pg = 0; pg < 2; ++pg)
+            for (int ks = 0; ks < 8; ++ks) {
+                const uint64_t a = umma::desc_k_sw128(QB + (ks >> 2) * 16384 + (ks & 3) * 32, 1024);
+                const uint64_t b = umma::desc_k_sw128(KB + pg * 4096 + (ks >> 2) * 2048 + (ks & 3) * 32, 1024);
+                umma::mma_ss(tmem + S_COL + pg * 16, a, b, id_s, ks > 0);
+            }
+        umma::commit(BAR);
+    }
+    const bool wg = warp >= 2;
+    const int row = 32 * (warp & 3) + lane;
+    const uint32_t lane_off = uint32_t(32 * (warp & 3)) << 16;
+    if (wg) {
+        mbar_wait(BAR, 0);
+        umma::fence_after();
+        float s[32];
+        umma::ld32(tmem + lane_off + S_COL, s);
+        umma::wait_ld();
+        uint32_t pk[16];
+        for (int i = 0; i < 32; ++i) out_s[row * 32 + i] = s[i];
+        for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(s[2 * i], s[2 * i + 1]);
+        umma::st16(tmem + lane_off + P_COL, pk);
+        umma::wait_st();
+        umma::fence_before();
+        mbar_arrive(BAR + 8);
+    }
+    if (tid == 32) {
+        mbar_wait(BAR + 8, 0);
+        umma::fence_after();
+        const uint32_t id_o = umma::idesc_bf16_f32(128, 128, false, true);
+        for (int pg = 0; pg < 2; ++pg)
+            umma::mma_ts(tmem + O_COL, tmem + P_COL + pg * 8, umma::desc_mn_sw128(VB + pg * 4096, 2048, 1024), id_o,
+                         pg > 0);
+        umma::commit(BAR + 16);
+    }
+    if (wg) {
+        mbar_wait(BAR + 16, 0);
+        umma::fence_after();
+        for (int c = 0; c < 4; ++c) {
+            float o[32];
+            umma::ld32(tmem + lane_off + O_COL + c * 32, o);
+            umma::wait_ld();
+            for (int i = 0; i < 32; ++i) out_o[row * 128 + c * 32 + i] = o[i];
+        }
+    }
+    umma::fence_before();
+    __syncthreads();
+    if (warp == 0) umma::tmem_dealloc(tmem, 256);
+}
+
 }  // namespace spa
 
 using namespace spa;
@@ -181,6 +271,20 @@ spa_status spa_debug_pool_read_tma(const spa_pool* pool, int32_t layers, int32_t
             : mode == 1 ? launch_probe<64, 1>(pool, mk, mv, units, pairs, s)
                         : launch_probe<64, 2>(pool, mk, mv, units, pairs, s);
     return e ? fail(SPA_ERR_CUDA, cudaGetErrorString(e)) : SPA_OK;
+}
+
+spa_status spa_debug_umma_selftest(const void* q, const void* k, const void* v, float* out_s, float* out_o,
+                                   void* stream) {
+    const int smem = 1024 + 32768 + 16384 + 128;
+    cudaError_t e = cudaFuncSetAttribute(spa::umma_selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) {
+        spa::umma_selftest_kernel<<<1, 192, smem, static_cast<cudaStream_t>(stream)>>>(
+            static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k),
+            static_cast<const __nv_bfloat16*>(v), out_s, out_o);
+        e = cudaGetLastError();
+    }
+    if (e != cudaSuccess) return spa::fail(SPA_ERR_CUDA, std::string("umma selftest: ") + cudaGetErrorString(e));
+    return SPA_OK;
 }
 
 }  // extern "C"

@@ -80,6 +80,7 @@ _SIGS = {
     "spa_debug_read_bw_ldg": (c_int32, [c_void_p, ctypes.c_size_t, c_void_p, c_void_p]),
     "spa_debug_pool_read_tma": (c_int32, [c_void_p, c_int32, c_int32, c_void_p]),
     "spa_debug_set_trace": (c_int32, [c_void_p, c_void_p, c_int32]),
+    "spa_debug_umma_selftest": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "spa_debug_plan_geometry": (c_int32, [c_void_p, P_int32, P_int32, P_int32]),
 }
 
@@ -119,6 +120,16 @@ def read_ceilings(pool: "Pool", scratch_bytes: int = 4 << 30, reps: int = 5, str
         out[name] = best
     out["tma_probe_bytes"] = layers * per_layer
     return out
+
+def umma_selftest(q, k, v, stream=None):
+    """tcgen05 descriptor/TMEM self-test (include/spa_debug.h): returns (S, O) fp32."""
+    import torch  # noqa: WPS433
+
+    s = torch.empty((128, 32), dtype=torch.float32, device=q.device)
+    o = torch.empty((128, 128), dtype=torch.float32, device=q.device)
+    _check(lib().spa_debug_umma_selftest(_ptr(q), _ptr(k), _ptr(v), _ptr(s), _ptr(o), _stream_ptr(stream)))
+    return s, o
+
 
 _lib = None
 
