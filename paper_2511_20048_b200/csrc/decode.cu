@@ -690,12 +690,14 @@ static int launch_decode_d(const spa_plan* P, const DecodeParams& dp, void* stre
 }
 
 bool decode_teams_supported(int mt, int teams) {
-    if (mt == 4) return teams == 1;
+    if (mt == 4 || mt == 8) return teams == 1;
     return teams == 1 || teams == 2 || (teams == 4 && mt == 1);
 }
 
 int launch_decode(const spa_plan* P, int32_t layer, const void* q, int64_t q_sr, int64_t q_sh, void* o, int64_t o_sr,
                   int64_t o_sh, float* lse, int64_t l_sr, int64_t l_sh, float scale, void* stream) {
+    if (P->mt == 8)   // 128-row items: the tcgen05 extend kernel (ext.cu)
+        return launch_ext(P, layer, q, q_sr, q_sh, o, o_sr, o_sh, lse, l_sr, l_sh, scale, stream);
     const auto& c = P->pool->cfg;
     const int32_t* H = P->host.data();
     if (H[H_N_ITEMS] == 0) return 0;

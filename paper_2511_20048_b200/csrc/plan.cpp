@@ -55,8 +55,10 @@ spa_status spa_plan_create(spa_pool* pool, const spa_plan_config* cfg, spa_plan*
     c.sharing = 1;
     if (cfg) c = *cfg;
     if (c.max_rows == 0) c.max_rows = 16;
-    if (c.max_rows != 16 && c.max_rows != 32 && c.max_rows != 64)
-        return fail(SPA_ERR_UNSUPPORTED, "max_rows must be 16, 32 or 64");
+    if (c.max_rows != 16 && c.max_rows != 32 && c.max_rows != 64 && c.max_rows != 128)
+        return fail(SPA_ERR_UNSUPPORTED, "max_rows must be 16, 32, 64 or 128");
+    if (c.max_rows == 128 && !ext_supported(pool->cfg.head_dim))
+        return fail(SPA_ERR_UNSUPPORTED, "max_rows 128 (tcgen05 extend kernel) needs head_dim 128");
     if (c.split_pages < 0 || c.num_ctas < 0) return fail(SPA_ERR_INVALID_ARG, "negative plan option");
     if (c.merge_mode < 0 || c.merge_mode > 2) return fail(SPA_ERR_INVALID_ARG, "merge_mode must be 0, 1 or 2");
     const int G = pool->cfg.num_q_heads / pool->cfg.num_kv_heads;
@@ -71,6 +73,8 @@ spa_status spa_plan_create(spa_pool* pool, const spa_plan_config* cfg, spa_plan*
     int teams = c.teams_per_cta;
     if (const char* e = std::getenv("SPA_TEAMS")) teams = std::atoi(e);
     if (teams == 0) teams = P->mt == 1 ? 4 : P->mt == 2 ? 2 : 1;
+    if (P->mt == 8 && c.merge_mode != 2 && c.merge_mode != 0)
+        return fail(SPA_ERR_UNSUPPORTED, "max_rows 128 merges split partials with the merge kernel");
     if (!decode_teams_supported(P->mt, teams)) {
         delete P;
         return fail(SPA_ERR_UNSUPPORTED, "teams_per_cta must be 1, 2 or 4 (4 only with max_rows 16, 1 with 64)");

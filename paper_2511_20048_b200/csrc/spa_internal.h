@@ -142,6 +142,10 @@ int launch_merge(int32_t n_req, int32_t num_heads, int32_t head_dim, const int32
                  const float* part_lse, void* o, int64_t o_sr, int64_t o_sh, float* lse, int64_t l_sr, int64_t l_sh,
                  int grid_hint, void* stream);
 bool decode_teams_supported(int mt, int teams);   // decode.cu: compiled (row tiles, teams/CTA)
+// ext.cu: the tcgen05 kernel for 128-row (extend) plans
+bool ext_supported(int head_dim);
+int launch_ext(const spa_plan* plan, int32_t layer, const void* q, int64_t q_sr, int64_t q_sh, void* o, int64_t o_sr,
+               int64_t o_sh, float* lse, int64_t l_sr, int64_t l_sh, float scale, void* stream);
 int memset_pool(spa_pool* pool);
 bool make_tensor_maps(spa_pool* pool, std::string* err);
 int device_sm_count(int* device_out);
