@@ -9,23 +9,53 @@
 //
 // One CTA per SM, warp-specialised:
 //   warp 0      producer: pops items from the plan's dynamic queue and streams each stage
-//               (2 pages of K and V of one KV head, 16 KB) into a 12-stage shared-memory
-//               ring with one 3-D TMA box per (page, tensor);
-//   warp 1      MMA issuer (one thread): S_j = Q K_j^T (per page: 8 x M128 N16 K16, A = the
-//               item's Q tile, K-major SW128; B = the K page as TMA wrote it), then
+//               (4 pages = 64 keys of K and V of one KV head, 32 KB) into a 5-stage
+//               shared-memory ring (TMA: K chunk by chunk so a stage's keys are contiguous,
+//               V one box per page);
+//   warp 1      MMA issuer (one elected lane): S_j = Q K_j^T (8 x M128 N64 K16, A = the
+//               item's Q tile, K-major SW128; B = the stage's keys), then
 //               O += P_{j-1} V_{j-1} (per page: M128 N128 K16, A = P in tensor memory,
 //               B = the V page as an MN-major SW128 operand);
-//   warps 2-5   softmax warpgroup, one thread per query row (tensor-memory lane): loads S_j,
-//               masks (window lo, causal hi, range end), runs the online softmax in the
-//               log2 domain with lazy rescaling of O (threshold 2^8, O rescaled in tensor
-//               memory), writes P_j (bf16) over S_j's columns, and at item end normalises
-//               O and writes bf16 O + LSE (or an fp32 partial record for split ranges).
-// S is double-buffered in tensor memory (2 x 32 columns), O takes 128 columns.
+//   warps 2-9   two softmax warpgroups, one thread per query row (tensor-memory lane) each;
+//               WG k takes the stages of parity k: loads S, masks (window lo, causal hi,
+//               range end), runs the online softmax in the log2 domain with lazy rescaling
+//               (threshold 2^8) of its own accumulator O_k in tensor memory, writes P (bf16)
+//               over S's columns; at item end the two (m, l, O_k) merge per row and bf16 O +
+//               LSE (or an fp32 partial record for split ranges) are written.
+// Tensor memory: S buffers 0-3 (64 columns each; PV lags S by 2 stages), O_0, O_1 (128 each).
 #include "device_util.cuh"
 #include "spa_internal.h"
 #include "umma.cuh"
 
 namespace spa {
+
+#ifdef SPA_EXT_DEBUG_HANG   // (debug builds: a wait that spins ~forever traps with its identity)
+__device__ int* g_ext_dbg;   // unused placeholder
+__device__ __forceinline__ void ext_wait(uint32_t bar, uint32_t parity, int id, const volatile int* dbg = nullptr) {
+    for (long long i = 0;; ++i) {
+        uint32_t ok;
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(bar), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (i == (1ll << 24)) {
+            printf("ext_kernel hang: block %d thread %d wait id %d parity %u bar %u | prod n %d slot %d st %d nst %d | mma n %d g %d st %d nst %d | wg g %d n %d\n",
+                   blockIdx.x, threadIdx.x, id, parity, (bar & 0xfff) >> 3, dbg ? dbg[0] : -1, dbg ? dbg[1] : -1,
+                   dbg ? dbg[2] : -1, dbg ? dbg[3] : -1, dbg ? dbg[4] : -1, dbg ? dbg[5] : -1, dbg ? dbg[6] : -1,
+                   dbg ? dbg[7] : -1, dbg ? dbg[8] : -1, dbg ? dbg[9] : -1);
+            __trap();
+        }
+    }
+}
+#define EXT_WAIT(b, ph, id) do { ext_wait(b, ph, id, dbgw); __syncwarp(); } while (0)
+#define EXT_DBG(i, v) (dbgw[i] = (v))
+#else
+// every wait reconverges its warp: the MMA issuer elects a lane right after waiting
+#define EXT_WAIT(b, ph, id) do { mbar_wait(b, ph); __syncwarp(); } while (0)
+#define EXT_DBG(i, v) ((void)0)
+#endif
 
 struct ExtParams {
     const int32_t* meta;
@@ -41,6 +71,8 @@ struct ExtParams {
     int layer_row_base;
     int num_q_heads, group_size, num_kv_heads;
     int launch;
+    unsigned long long* trace;   // spa_debug_set_trace: per-warp events of CTA 0 (stage timeline)
+    int trace_cap;
 };
 
 struct ExtItem {
@@ -50,24 +82,39 @@ struct ExtItem {
 namespace ext {
 constexpr int D = 128;
 constexpr int PAGE_BYTES = kPageSize * D * 2;     // 4 KB: K (or V) of one page, one head
-constexpr int STAGE_BYTES = 2 * 2 * PAGE_BYTES;   // 2 pages x (K, V)
-constexpr int NS = 12;                            // ring stages
-constexpr int QN = NS + 2;                        // popped-item queue entries
+#ifndef SPA_EXT_PPS
+#define SPA_EXT_PPS 4
+#endif
+constexpr int PPS = SPA_EXT_PPS;                  // pages per stage
+constexpr int KPS = PPS * kPageSize;              // keys per stage (S columns)
+constexpr int STAGE_BYTES = PPS * 2 * PAGE_BYTES; // PPS pages x (K, V)
+// stage layout: K key-contiguous [2 chunks][KPS rows][128 B] (one MMA covers every key of the
+// stage: N = KPS), then V page by page [page][2 chunks][16 rows][128 B] (one K=16 MMA each)
+constexpr int K_CHUNK = KPS * 128;                // bytes per 64-column chunk of the stage's keys
+constexpr int OFF_V = 2 * K_CHUNK;
+constexpr int NS = (232448 - 1024 - 32768 - 4096) / STAGE_BYTES;   // ring stages
+constexpr int QN = NS + 8;   // popped-item queue entries: the producer runs up to NS + LAG + 1
+                              // stages (items, when items are one stage long) ahead of the WGs
 constexpr int OFF_Q = NS * STAGE_BYTES;           // Q tile: 2 chunks x 128 rows x 128 B
 constexpr int OFF_BAR = OFF_Q + 32768;
-// barriers: full[NS], empty[NS], s_full[2], p_full[2], q_ready, o_full, pv_done
-constexpr int BAR_FULL = 0, BAR_EMPTY = NS, BAR_SFULL = 2 * NS, BAR_PFULL = 2 * NS + 2, BAR_QREADY = 2 * NS + 4,
-              BAR_OFULL = 2 * NS + 5, BAR_PVDONE = 2 * NS + 6, N_BARS = 2 * NS + 7;
+// barriers: full[NS], empty[NS], s_full[4], p_full[4] (one per S buffer: a buffer's next
+// S / P needs this round's P / S, so each barrier is at most one phase ahead of its waiter),
+// q_ready, o_full, pv_done[4] (PV of the stages using S buffer b)
+constexpr int BAR_FULL = 0, BAR_EMPTY = NS, BAR_SFULL = 2 * NS, BAR_PFULL = 2 * NS + 4, BAR_QREADY = 2 * NS + 8,
+              BAR_OFULL = 2 * NS + 9, BAR_PVDONE = 2 * NS + 10, N_BARS = 2 * NS + 14;
 constexpr int OFF_TQ = OFF_BAR + N_BARS * 8;
-constexpr int OFF_TSLOT = OFF_TQ + QN * int(sizeof(ExtItem));
-constexpr int SMEM = 1024 + OFF_TSLOT + 16;
-constexpr int THREADS = 192;
-constexpr uint32_t TMEM_COLS = 256, S_COL = 0, O_COL = 128;
+constexpr int OFF_ML = (OFF_TQ + QN * int(sizeof(ExtItem)) + 15) & ~15;   // [2][2][128] fp32 + 8 flags
+constexpr int OFF_TSLOT = OFF_ML + 4 * 128 * 4 + 8 * 4;
+constexpr int SMEM = 1024 + OFF_TSLOT + 16 + 128;   // + debug words (hang-trap builds)
+constexpr int THREADS = 320;                       // producer, MMA issuer, 2 softmax warpgroups
+// tensor memory: S buffers 0..3 (KPS columns each; stage g uses g % 4), O_0, O_1 (128 each)
+constexpr uint32_t TMEM_COLS = 512, S_COL = 0, O_COL = 256;
+static_assert(4 * KPS <= int(O_COL), "S buffers overlap O");
 static_assert(SMEM <= 232448, "extend kernel shared memory");
 }  // namespace ext
 
 __global__ void __launch_bounds__(ext::THREADS, 1)
-    ext_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv, const ExtParams p) {
+    ext_kernel(const __grid_constant__ CUtensorMap tmk1, const __grid_constant__ CUtensorMap tmv, const ExtParams p) {
     using namespace ext;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -76,19 +123,22 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
     const int lane = threadIdx.x & 31;
     auto bar = [&](int i) { return sbase + OFF_BAR + i * 8; };
     ExtItem* tq = reinterpret_cast<ExtItem*>(smem + OFF_TQ);
+#ifdef SPA_EXT_DEBUG_HANG
+    volatile int* dbgw = reinterpret_cast<volatile int*>(smem + OFF_TSLOT + 64);   // past the TMEM slot
+#endif
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < NS; ++i) {
             mbar_init(bar(BAR_FULL + i), 1);
             mbar_init(bar(BAR_EMPTY + i), 1);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < 4; ++b) {
             mbar_init(bar(BAR_SFULL + b), 1);
             mbar_init(bar(BAR_PFULL + b), 128);
+            mbar_init(bar(BAR_PVDONE + b), 1);
         }
-        mbar_init(bar(BAR_QREADY), 128);
+        mbar_init(bar(BAR_QREADY), 256);
         mbar_init(bar(BAR_OFULL), 1);
-        mbar_init(bar(BAR_PVDONE), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) umma::tmem_alloc(sbase + OFF_TSLOT, TMEM_COLS);
@@ -97,6 +147,20 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
     umma::fence_after();
     const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + OFF_TSLOT);
     asm volatile("griddepcontrol.launch_dependents;");
+    // stage timeline of CTA 0 (spa_debug_set_trace): lane 0 of warps 0..2 records (tag, clock64)
+    unsigned long long* trace = (p.trace && blockIdx.x == 0 && warp <= 2 && lane == 0)
+                                    ? p.trace + 2ull * warp * p.trace_cap : nullptr;
+    int tr_n = 0;
+    auto tr = [&](unsigned long long tag, int id) {
+        if (trace && tr_n < p.trace_cap) {
+            unsigned long long gt, ck;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+            asm volatile("mov.u64 %0, %%clock64;" : "=l"(ck));
+            trace[2 * tr_n] = gt;
+            trace[2 * tr_n + 1] = (tag << 56) | ((unsigned long long)(id & 0xffffff) << 32) | (ck & 0xffffffffull);
+            ++tr_n;
+        }
+    };
 
     const int32_t* meta = p.meta;
     const Desc* descs = reinterpret_cast<const Desc*>(meta + meta[H_OFF_DESC]);
@@ -129,7 +193,7 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
             ExtItem* e = &tq[n % QN];
             ++n;
             // the ring slot for this item's first stage (or the end marker)
-            mbar_wait(bar(BAR_EMPTY + slot), ph ^ 1u);
+            EXT_WAIT(bar(BAR_EMPTY + slot), ph ^ 1u, 1);
             if (it < 0) {
                 if (lane == 0) {
                     e->it = -1;
@@ -148,13 +212,14 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
             }
             int pid_cur = lane < dsc.n_pages ? pages[dsc.page_off + lane] : 0;
             int pid_base = 0;
-            const int nst = (dsc.n_pages + 1) / 2;
+            const int nst = (dsc.n_pages + PPS - 1) / PPS;
             for (int st = 0; st < nst; ++st) {
-                if (st > 0) mbar_wait(bar(BAR_EMPTY + slot), ph ^ 1u);
-                const int p0 = st * 2, npg = min(2, dsc.n_pages - p0);
-                int row[2];
+                if (st > 0) EXT_WAIT(bar(BAR_EMPTY + slot), ph ^ 1u, 2);
+                tr(10, st);
+                const int p0 = st * PPS, npg = min(PPS, dsc.n_pages - p0);
+                int row[PPS];
 #pragma unroll
-                for (int j = 0; j < 2; ++j) {
+                for (int j = 0; j < PPS; ++j) {
                     const int kk = p0 + j;
                     if (kk >= pid_base + 32) {
                         pid_base += 32;
@@ -168,11 +233,18 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
                     mbar_expect_tx(fb, npg * 2 * PAGE_BYTES);
                     const uint32_t sb = sbase + slot * STAGE_BYTES;
                     for (int j = 0; j < npg; ++j) {
-                        tma_load_3d(sb + j * 2 * PAGE_BYTES, &tmk, 0, row[j], 0, fb, policy);
-                        tma_load_3d(sb + j * 2 * PAGE_BYTES + PAGE_BYTES, &tmv, 0, row[j], 0, fb, policy);
+                        tma_load_3d(sb + j * 2048, &tmk1, 0, row[j], 0, fb, policy);
+                        tma_load_3d(sb + K_CHUNK + j * 2048, &tmk1, 0, row[j], 1, fb, policy);
+                        tma_load_3d(sb + OFF_V + j * PAGE_BYTES, &tmv, 0, row[j], 0, fb, policy);
                     }
                 }
                 __syncwarp();
+                if (lane == 0) {
+                    EXT_DBG(0, n);
+                    EXT_DBG(1, slot);
+                    EXT_DBG(2, st);
+                    EXT_DBG(3, nst);
+                }
                 if (++slot == NS) {
                     slot = 0;
                     ph ^= 1u;
@@ -181,95 +253,119 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
-            const uint32_t id_s = umma::idesc_bf16_f32(128, 16, false, false);
-            const uint32_t id_o = umma::idesc_bf16_f32(128, 128, false, true);
-            const uint32_t QB = sbase + OFF_Q;
-            int slot = 0, n = 0;
-            uint32_t ph = 0, qph = 0;
-            uint32_t pph[2] = {0, 0};
-            int g = 0;   // running stage counter (S buffer = g & 1)
-            while (true) {
-                mbar_wait(bar(BAR_FULL + slot), ph);
-                const ExtItem e = tq[n % QN];
-                ++n;
-                if (e.it < 0) break;
-                mbar_wait(bar(BAR_QREADY), qph);   // Q tile written (and the last item's O read out)
-                qph ^= 1u;
-                umma::fence_after();
-                const int nst = (e.n_pages + 1) / 2;
-                int prev_slot = 0, prev_npg = 0;
-                for (int st = 0; st < nst; ++st, ++g) {
-                    if (st > 0) mbar_wait(bar(BAR_FULL + slot), ph);
-                    umma::fence_after();
-                    const int npg = min(2, e.n_pages - st * 2);
-                    const uint32_t sb = sbase + slot * STAGE_BYTES;
-                    const uint32_t sbuf = tmem + S_COL + (g & 1) * 32;
-                    for (int pg = 0; pg < npg; ++pg)
-#pragma unroll
-                        for (int ks = 0; ks < D / 16; ++ks) {
-                            const uint64_t a = umma::desc_k_sw128(QB + (ks >> 2) * 16384 + (ks & 3) * 32, 1024);
-                            const uint64_t b =
-                                umma::desc_k_sw128(sb + pg * 2 * PAGE_BYTES + (ks >> 2) * 2048 + (ks & 3) * 32, 1024);
-                            umma::mma_ss(sbuf + pg * 16, a, b, id_s, ks > 0);
-                        }
-                    umma::commit(bar(BAR_SFULL + (g & 1)));
-                    if (st > 0) {   // O += P_{g-1} V_{g-1}
-                        const int b = (g - 1) & 1;
-                        mbar_wait(bar(BAR_PFULL + b), pph[b]);
-                        pph[b] ^= 1u;
-                        umma::fence_after();
-                        const uint32_t psb = sbase + prev_slot * STAGE_BYTES;
-                        for (int pg = 0; pg < prev_npg; ++pg)
-                            umma::mma_ts(tmem + O_COL, tmem + S_COL + b * 32 + pg * 8,
-                                         umma::desc_mn_sw128(psb + pg * 2 * PAGE_BYTES + PAGE_BYTES, 2048, 1024), id_o,
-                                         st > 1 || pg > 0);
-                        umma::commit(bar(BAR_EMPTY + prev_slot));
-                        umma::commit(bar(BAR_PVDONE));
-                    }
-                    prev_slot = slot;
-                    prev_npg = npg;
-                    if (++slot == NS) {
-                        slot = 0;
-                        ph ^= 1u;
-                    }
+        // The whole warp walks the pipeline (its values stay warp-uniform, so descriptors
+        // live in uniform registers); one elected lane issues each batch of MMAs + commits.
+        const uint32_t id_o = umma::idesc_bf16_f32(128, 128, false, true);
+        const uint64_t q_desc = umma::desc_k_sw128(sbase + OFF_Q, 1024);
+        int slot = 0, n = 0;
+        uint32_t ph = 0, qph = 0;
+        uint32_t pph[4] = {0, 0, 0, 0};
+        int g = 0;   // running stage counter (S buffer = g & 1)
+        bool o_written[2] = {false, false};   // O_k has received a PV in this item
+        // PV of a stage is issued LAG stages after its S (S_g is queued before P_{g-2} is
+        // awaited), so each softmax warpgroup finds its next S ready when it finishes one
+        constexpr int LAG = 2;
+        int lag_slot[LAG + 1], lag_npg[LAG + 1], lag_g[LAG + 1];   // pending stages (one pushed before a retire)
+        int n_lag = 0;
+        auto retire = [&]() {   // wait for the oldest pending stage's P, then O_b += P V
+            const int gg = lag_g[0], b = gg & 1, ps = lag_slot[0], pn = lag_npg[0];
+            EXT_WAIT(bar(BAR_PFULL + (gg & 3)), pph[gg & 3], 7);
+            pph[gg & 3] ^= 1u;
+            umma::fence_after();
+            const uint64_t v_desc = umma::desc_mn_sw128(sbase + ps * STAGE_BYTES + OFF_V, 2048, 1024);
+            if (umma::elect_one()) {
+                for (int pg = 0; pg < pn; ++pg)
+                    umma::mma_ts(tmem + O_COL + b * 128, tmem + S_COL + (gg & 3) * KPS + pg * 8,
+                                 v_desc + uint64_t((pg * PAGE_BYTES) >> 4), id_o, o_written[b] || pg > 0);
+                umma::commit(bar(BAR_EMPTY + ps));
+                umma::commit(bar(BAR_PVDONE + (gg & 3)));
+            }
+            __syncwarp();
+            o_written[b] = true;
+            for (int i = 0; i + 1 < n_lag; ++i) {
+                lag_slot[i] = lag_slot[i + 1];
+                lag_npg[i] = lag_npg[i + 1];
+                lag_g[i] = lag_g[i + 1];
+            }
+            --n_lag;
+        };
+        while (true) {
+            EXT_WAIT(bar(BAR_FULL + slot), ph, 3);
+            const ExtItem e = tq[n % QN];
+            ++n;
+            if (e.it < 0) break;
+            EXT_WAIT(bar(BAR_QREADY), qph, 4);   // Q tile written (and the last item's O read out)
+            qph ^= 1u;
+            umma::fence_after();
+            o_written[0] = o_written[1] = false;
+            const int nst = (e.n_pages + PPS - 1) / PPS;
+            for (int st = 0; st < nst; ++st, ++g) {
+                if (lane == 0) {
+                    EXT_DBG(4, n);
+                    EXT_DBG(5, g);
+                    EXT_DBG(6, st);
+                    EXT_DBG(7, nst);
                 }
-                {   // the item's last PV, then O is complete
-                    const int b = (g - 1) & 1;
-                    mbar_wait(bar(BAR_PFULL + b), pph[b]);
-                    pph[b] ^= 1u;
-                    umma::fence_after();
-                    const uint32_t psb = sbase + prev_slot * STAGE_BYTES;
-                    for (int pg = 0; pg < prev_npg; ++pg)
-                        umma::mma_ts(tmem + O_COL, tmem + S_COL + b * 32 + pg * 8,
-                                     umma::desc_mn_sw128(psb + pg * 2 * PAGE_BYTES + PAGE_BYTES, 2048, 1024), id_o,
-                                     nst > 1 || pg > 0);
-                    umma::commit(bar(BAR_EMPTY + prev_slot));
-                    umma::commit(bar(BAR_OFULL));
+                if (st > 0) EXT_WAIT(bar(BAR_FULL + slot), ph, 5);
+                tr(20, st);
+                umma::fence_after();
+                const int npg = min(PPS, e.n_pages - st * PPS);
+                const uint64_t k_desc = umma::desc_k_sw128(sbase + slot * STAGE_BYTES, 1024);
+                const uint32_t sbuf = tmem + S_COL + (g & 3) * KPS;
+                const uint32_t id_s = umma::idesc_bf16_f32(128, npg * 16, false, false);
+                if (umma::elect_one()) {
+#pragma unroll
+                    for (int ks = 0; ks < D / 16; ++ks)   // 16-B units: chunk stride, 32 B per K step
+                        umma::mma_ss(sbuf, q_desc + uint64_t((ks >> 2) * (16384 >> 4) + (ks & 3) * 2),
+                                     k_desc + uint64_t((ks >> 2) * (K_CHUNK >> 4) + (ks & 3) * 2), id_s, ks > 0);
+                    umma::commit(bar(BAR_SFULL + (g & 3)));
+                }
+                __syncwarp();
+                tr(21, st);
+                lag_slot[n_lag] = slot;
+                lag_npg[n_lag] = npg;
+                lag_g[n_lag] = g;
+                ++n_lag;
+                if (n_lag > LAG) retire();
+                if (++slot == NS) {
+                    slot = 0;
+                    ph ^= 1u;
                 }
             }
+            while (n_lag > 0) retire();   // the item's last PVs, then O is complete
+            if (umma::elect_one()) umma::commit(bar(BAR_OFULL));
+            __syncwarp();
         }
-        __syncwarp();
     } else {
-        // ------------------------------------------------------------ softmax warpgroup
+        // ------------------------------------------------------------ softmax warpgroups
+        // WG k (warps 2 + 4k .. 5 + 4k) takes the stages of parity k (global stage counter)
+        // with its own running (m, l) and its own O accumulator O_k; PV of stage g adds into
+        // O_{g & 1}, so a WG's O is stable whenever its S_g has landed (S_g was issued after
+        // PV_{g-2}) and rescaling needs no extra wait.  At item end the two halves merge.
+        const int wgk = (warp - 2) >> 2;
         const int row = 32 * (warp & 3) + lane;          // query row = tensor-memory lane
         const uint32_t lane_off = uint32_t(32 * (warp & 3)) << 16;
-        const uint32_t q_row = smem_u32(smem + OFF_Q);
+        const uint32_t o_mine = tmem + lane_off + O_COL + wgk * 128;
+        float* ml = reinterpret_cast<float*>(smem + OFF_ML);   // [2 WGs][2][128]: m, l per row
         asm volatile("griddepcontrol.wait;" ::: "memory");   // q and the outputs belong to the stream
-        int slot = 0, n = 0, g = 0;
-        uint32_t ph = 0, oph = 0, pvph = 0;
-        uint32_t sph[2] = {0, 0};
+        int n = 0, g = 0;   // g: global stage counter (ring slot g % NS, phase (g / NS) & 1)
+        uint32_t oph = 0, sph[2] = {0, 0};   // phases of this WG's S buffers k, k + 2
         constexpr float kRescale = 8.f;
+        auto wg_sync = [&]() { asm volatile("bar.sync 1, 256;" ::: "memory"); };
         while (true) {
-            mbar_wait(bar(BAR_FULL + slot), ph);   // the item's first stage landed: its entry is valid
+            // the item's first stage landed: its entry is valid.  Only the first stage's
+            // slot is awaited here (its next fill needs this item's P, so it cannot run
+            // ahead); the other stages are tracked through s_full.
+            EXT_WAIT(bar(BAR_FULL + g % NS), uint32_t((g / NS) & 1), 8);
             const ExtItem e = tq[n % QN];
             ++n;
             if (e.it < 0) break;
             const int R = e.n_members * G;
-            // ---- row setup + Q tile (K-major SW128: chunk c of row r at c * 16 KB + sw128(r, u))
+            // ---- row setup + this WG's half of the Q tile (K-major SW128: 64-column chunk
+            //      c = wgk of row r at c * 16 KB + sw128(r, u))
             int lo = 0, hi = 0, mrow = 0, rec = -1, head = 0;
             const bool live = row < R;
-            uint4 qv[16];
+            uint4 qv[8];
             if (live) {
                 const int mb = row / G;
                 const Member m = mems[e.member_off + mb];
@@ -278,118 +374,161 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
                 mrow = m.row;
                 rec = m.rec;
                 head = e.kv_head * G + (row - mb * G);
-                const uint4* src = reinterpret_cast<const uint4*>(p.q + m.row * p.q_sr + head * p.q_sh);
+                const uint4* src = reinterpret_cast<const uint4*>(p.q + m.row * p.q_sr + head * p.q_sh) + wgk * 8;
 #pragma unroll
-                for (int u = 0; u < 16; ++u) qv[u] = src[u];
+                for (int u = 0; u < 8; ++u) qv[u] = src[u];
             } else {
 #pragma unroll
-                for (int u = 0; u < 16; ++u) qv[u] = make_uint4(0u, 0u, 0u, 0u);
+                for (int u = 0; u < 8; ++u) qv[u] = make_uint4(0u, 0u, 0u, 0u);
             }
 #pragma unroll
-            for (int u = 0; u < 16; ++u)
-                *reinterpret_cast<uint4*>(smem + OFF_Q + (u >> 3) * 16384 + umma::sw128_offset(row, u & 7)) = qv[u];
+            for (int u = 0; u < 8; ++u)
+                *reinterpret_cast<uint4*>(smem + OFF_Q + wgk * 16384 + umma::sw128_offset(row, u)) = qv[u];
             umma::fence_proxy_async_smem();
             mbar_arrive(bar(BAR_QREADY));
-            (void)q_row;
 
             float m_run = -INFINITY, l_run = 0.f;
-            const int nst = (e.n_pages + 1) / 2;
+            bool mine_any = false;   // did this WG take a stage of the item (O_k written)?
+            const int nst = (e.n_pages + PPS - 1) / PPS;
             for (int st = 0; st < nst; ++st, ++g) {
-                const int b = g & 1;
-                mbar_wait(bar(BAR_SFULL + b), sph[b]);
-                sph[b] ^= 1u;
-                umma::fence_after();
-                float s[32];
-                umma::ld32(tmem + lane_off + S_COL + b * 32, s);
-                umma::wait_ld();
-                const int npg = min(2, e.n_pages - st * 2);
-                const int tok0 = e.tok_start + st * 32;
-                const int kmax = min(min(hi, e.tok_end), tok0 + npg * 16);   // keys [max(lo,tok0), kmax) live
-                float mx = -INFINITY;
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    const int tok = tok0 + i;
-                    const float v = (tok < kmax && tok >= lo) ? s[i] * p.scale_log2 : -INFINITY;
-                    s[i] = v;
-                    mx = fmaxf(mx, v);
+                if (threadIdx.x == 64) {
+                    EXT_DBG(8, g);
+                    EXT_DBG(9, n);
                 }
-                if (st > 0) {   // O holds P_{<st} V: PV of the previous stage must be complete
-                    mbar_wait(bar(BAR_PVDONE), pvph);
-                    pvph ^= 1u;
-                }
-                // lazy rescale (P <= 2^kRescale), decided per warp: tensor-memory loads and
-                // stores are warp-collective, so a warp rescales all its rows together
-                const bool grow = mx > m_run + kRescale || (m_run == -INFINITY && mx > -INFINITY);
-                if (__any_sync(0xffffffffu, grow)) {
-                    const float mn = fmaxf(m_run, mx);
-                    const float al = (m_run == -INFINITY) ? 0.f : fast_exp2(m_run - mn);
-                    l_run *= al;
-                    m_run = mn;
-                    if (st > 0) {
-                        umma::fence_after();
-#pragma unroll 1
-                        for (int c = 0; c < 4; ++c) {
-                            float ov[32];
-                            umma::ld32(tmem + lane_off + O_COL + c * 32, ov);
-                            umma::wait_ld();
+                if ((g & 1) == wgk) {
+                    EXT_WAIT(bar(BAR_SFULL + (g & 3)), sph[(g >> 1) & 1], 9);
+                    sph[(g >> 1) & 1] ^= 1u;
+                    tr(30, st);
+                    umma::fence_after();
+                    float s[KPS];
 #pragma unroll
-                            for (int i = 0; i < 32; ++i) ov[i] *= al;
-                            umma::st32(tmem + lane_off + O_COL + c * 32, ov);
+                    for (int c = 0; c < KPS / 32; ++c)
+                        umma::ld32(tmem + lane_off + S_COL + (g & 3) * KPS + c * 32, s + c * 32);
+                    umma::wait_ld();
+                    const int npg = min(PPS, e.n_pages - st * PPS);
+                    const int tok0 = e.tok_start + st * KPS;
+                    const int kmax = min(min(hi, e.tok_end), tok0 + npg * 16);   // keys [max(lo,tok0), kmax) live
+                    float mx = -INFINITY;   // max of the raw logits (scale > 0 is applied in the exponent)
+                    if (tok0 >= lo && tok0 + KPS <= kmax) {
+#pragma unroll
+                        for (int i = 0; i < KPS; ++i) mx = fmaxf(mx, s[i]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < KPS; ++i) {
+                            const int tok = tok0 + i;
+                            s[i] = (tok < kmax && tok >= lo) ? s[i] : -INFINITY;
+                            mx = fmaxf(mx, s[i]);
                         }
-                        umma::wait_st();
                     }
-                }
-                const float mu = m_run == -INFINITY ? 0.f : m_run;
-                uint32_t pk[16];
+                    mx *= p.scale_log2;
+                    // lazy rescale (P <= 2^kRescale), decided per warp: tensor-memory loads and
+                    // stores are warp-collective, so a warp rescales all its rows together
+                    const bool grow = mx > m_run + kRescale || (m_run == -INFINITY && mx > -INFINITY);
+                    if (__any_sync(0xffffffffu, grow)) {
+                        const float mn = fmaxf(m_run, mx);
+                        const float al = (m_run == -INFINITY) ? 0.f : fast_exp2(m_run - mn);
+                        l_run *= al;
+                        m_run = mn;
+                        if (mine_any) {   // O_k holds this WG's earlier stages
+                            // PV of this WG's previous stage g - 2 may still run (PV lags S by
+                            // LAG = 2): wait for it.  pv_done[(g-2) % 4] completes once per 4
+                            // stages; PV g-6 is complete (issued before S g) and PV g+2 needs
+                            // P g, so the parity of completion (g-2) / 4 is exact.
+                            EXT_WAIT(bar(BAR_PVDONE + ((g - 2) & 3)), uint32_t(((g - 2) >> 2) & 1), 10);
+                            umma::fence_after();
+#pragma unroll 1
+                            for (int c = 0; c < 4; ++c) {
+                                float ov[32];
+                                umma::ld32(o_mine + c * 32, ov);
+                                umma::wait_ld();
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const float e0 = fast_exp2(s[2 * i] - mu), e1 = fast_exp2(s[2 * i + 1] - mu);
-                    l_run += e0 + e1;
-                    pk[i] = pack_bf16(e0, e1);
+                                for (int i = 0; i < 32; ++i) ov[i] *= al;
+                                umma::st32(o_mine + c * 32, ov);
+                            }
+                            umma::wait_st();
+                        }
+                    }
+                    const float mu = m_run == -INFINITY ? 0.f : m_run;
+                    uint32_t pk[KPS / 2];
+                    float lp[4] = {0.f, 0.f, 0.f, 0.f};   // independent partial sums (short add chains)
+#pragma unroll
+                    for (int i = 0; i < KPS / 2; ++i) {
+                        const float e0 = fast_exp2(fmaf(s[2 * i], p.scale_log2, -mu));
+                        const float e1 = fast_exp2(fmaf(s[2 * i + 1], p.scale_log2, -mu));
+                        lp[i & 3] += e0 + e1;
+                        pk[i] = pack_bf16(e0, e1);
+                    }
+                    l_run += (lp[0] + lp[1]) + (lp[2] + lp[3]);
+#pragma unroll
+                    for (int c = 0; c < KPS / 32; ++c)
+                        umma::st16(tmem + lane_off + S_COL + (g & 3) * KPS + c * 16, pk + c * 16);
+                    umma::wait_st();
+                    umma::fence_before();
+                    mbar_arrive(bar(BAR_PFULL + (g & 3)));
+                    tr(31, st);
+                    mine_any = true;
                 }
-                umma::st16(tmem + lane_off + S_COL + b * 32, pk);
-                umma::wait_st();
-                umma::fence_before();
-                mbar_arrive(bar(BAR_PFULL + b));
-                if (++slot == NS) {
-                    slot = 0;
-                    ph ^= 1u;
-                }
-                if (st + 1 < nst) mbar_wait(bar(BAR_FULL + slot), ph);   // keep the item walk in step
             }
-            // ---- epilogue: O complete in tensor memory
-            mbar_wait(bar(BAR_OFULL), oph);
+            // ---- epilogue: both O halves complete; merge the two WGs' softmax states per row
+            EXT_WAIT(bar(BAR_OFULL), oph, 6);
             oph ^= 1u;
             umma::fence_after();
-            const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-            const float lse = l_run > 0.f ? (m_run + log2f(l_run)) * 0.69314718055994531f : -INFINITY;
+            ml[(wgk * 2 + 0) * 128 + row] = m_run;
+            ml[(wgk * 2 + 1) * 128 + row] = l_run;
+            const uint32_t used = __ballot_sync(0xffffffffu, mine_any);   // uniform per WG
+            if (lane == 0) reinterpret_cast<volatile uint32_t*>(ml + 512)[warp - 2] = used != 0;
+            wg_sync();
+            const float m0 = ml[row], l0 = ml[128 + row], m1 = ml[256 + row], l1 = ml[384 + row];
+            const bool have0 = reinterpret_cast<volatile uint32_t*>(ml + 512)[(warp & 3) ^ 2] != 0;   // WG0 warp, same lanes
+            const bool have1 = reinterpret_cast<volatile uint32_t*>(ml + 512)[4 + ((warp & 3) ^ 2)] != 0;
+            const float M = fmaxf(m0, m1);
+            const float a0 = m0 == -INFINITY ? 0.f : fast_exp2(m0 - M), a1 = m1 == -INFINITY ? 0.f : fast_exp2(m1 - M);
+            const float L = l0 * a0 + l1 * a1;
+            const float inv = L > 0.f ? 1.f / L : 0.f;
+            const float w0 = a0 * inv, w1 = a1 * inv;
+            // WG k writes output columns [64 k, 64 k + 64)
 #pragma unroll 1
-            for (int c = 0; c < 4; ++c) {   // warp-collective loads; live rows store
-                float ov[32];
-                umma::ld32(tmem + lane_off + O_COL + c * 32, ov);
+            for (int c = 0; c < 2; ++c) {
+                const int col = wgk * 64 + c * 32;
+                float o0[32], o1[32];
+                if (have0) {
+                    umma::ld32(tmem + lane_off + O_COL + col, o0);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) o0[i] = 0.f;
+                }
+                if (have1) {
+                    umma::ld32(tmem + lane_off + O_COL + 128 + col, o1);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) o1[i] = 0.f;
+                }
                 umma::wait_ld();
+#pragma unroll
+                for (int i = 0; i < 32; ++i) o0[i] = o0[i] * w0 + o1[i] * w1;
                 if (live && rec < 0) {
-                    uint4* dst = reinterpret_cast<uint4*>(p.o + mrow * p.o_sr + head * p.o_sh + c * 32);
+                    uint4* dst = reinterpret_cast<uint4*>(p.o + mrow * p.o_sr + head * p.o_sh + col);
 #pragma unroll
                     for (int u = 0; u < 4; ++u)
-                        dst[u] = make_uint4(pack_bf16(ov[8 * u] * inv, ov[8 * u + 1] * inv),
-                                            pack_bf16(ov[8 * u + 2] * inv, ov[8 * u + 3] * inv),
-                                            pack_bf16(ov[8 * u + 4] * inv, ov[8 * u + 5] * inv),
-                                            pack_bf16(ov[8 * u + 6] * inv, ov[8 * u + 7] * inv));
+                        dst[u] = make_uint4(pack_bf16(o0[8 * u], o0[8 * u + 1]), pack_bf16(o0[8 * u + 2], o0[8 * u + 3]),
+                                            pack_bf16(o0[8 * u + 4], o0[8 * u + 5]),
+                                            pack_bf16(o0[8 * u + 6], o0[8 * u + 7]));
                 } else if (live) {
-                    float4* dst = reinterpret_cast<float4*>(p.part_o + ((long long)rec * Hq + head) * D + c * 32);
+                    float4* dst = reinterpret_cast<float4*>(p.part_o + ((long long)rec * Hq + head) * D + col);
 #pragma unroll
-                    for (int u = 0; u < 8; ++u)
-                        dst[u] =
-                            make_float4(ov[4 * u] * inv, ov[4 * u + 1] * inv, ov[4 * u + 2] * inv, ov[4 * u + 3] * inv);
+                    for (int u = 0; u < 8; ++u) dst[u] = make_float4(o0[4 * u], o0[4 * u + 1], o0[4 * u + 2], o0[4 * u + 3]);
                 }
             }
-            if (live && rec < 0) {
-                if (p.lse) p.lse[mrow * p.l_sr + head * p.l_sh] = lse;
-            } else if (live) {
-                p.part_lse[(long long)rec * Hq + head] = lse;
+            if (wgk == 0 && live) {
+                const float lse = L > 0.f ? (M + log2f(L)) * 0.69314718055994531f : -INFINITY;
+                if (rec < 0) {
+                    if (p.lse) p.lse[mrow * p.l_sr + head * p.l_sh] = lse;
+                } else {
+                    p.part_lse[(long long)rec * Hq + head] = lse;
+                }
             }
             umma::fence_before();
+            wg_sync();   // ml is rewritten at the next item's end; O is free for the next item
         }
     }
 
@@ -444,7 +583,9 @@ int launch_ext(const spa_plan* P, int32_t layer, const void* q, int64_t q_sr, in
     ep.num_kv_heads = c.num_kv_heads;
     ep.group_size = c.num_q_heads / c.num_kv_heads;
     ep.launch = int(P->launches++);
-    const CUtensorMap* tk = reinterpret_cast<const CUtensorMap*>(P->pool->tmap_k.bytes);
+    ep.trace = P->trace;
+    ep.trace_cap = P->trace_cap;
+    const CUtensorMap* tk = reinterpret_cast<const CUtensorMap*>(P->pool->tmap_k1.bytes);
     const CUtensorMap* tv = reinterpret_cast<const CUtensorMap*>(P->pool->tmap_v.bytes);
     int err = launch_pdl(ext_kernel, dim3(P->num_ctas), dim3(ext::THREADS), ext::SMEM, stream, *tk, *tv, ep);
     if (err) return err;

@@ -82,10 +82,12 @@ bool make_tensor_maps(spa_pool* p, std::string* err) {
     cuuint32_t estr[3] = {1, 1, 1};
     void* ptrs[2] = {p->k_pool, p->v_pool};
     spa_tmap* maps[2] = {&p->tmap_k, &p->tmap_v};
-    for (int i = 0; i < 2; ++i) {
-        CUresult r = enc(reinterpret_cast<CUtensorMap*>(maps[i]->bytes), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, ptrs[i],
-                         dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    for (int i = 0; i < 3; ++i) {
+        cuuint32_t bx[3] = {box[0], box[1], i < 2 ? box[2] : 1u};
+        CUresult r = enc(reinterpret_cast<CUtensorMap*>(i < 2 ? maps[i]->bytes : p->tmap_k1.bytes),
+                         CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, i < 2 ? ptrs[i] : p->k_pool, dims, strides, bx, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) {
             *err = "CUresult " + std::to_string(int(r));
             return false;

@@ -96,6 +96,7 @@ struct spa_pool {
     std::vector<int32_t> refcount;
     std::set<int32_t> free_set;
     spa_tmap tmap_k, tmap_v;
+    spa_tmap tmap_k1;   // K pool, one 64-column chunk per box (the extend kernel's key-contiguous stages)
 };
 
 struct spa_plan {

@@ -43,3 +43,17 @@ def test_tc_matches_mma_sync_path():
     _ok(e2)
     d = (a[0][0].float() - b[0][0].float()).abs().max().item()
     assert d <= 1.6e-2, d
+
+
+@pytest.mark.parametrize("split", [0, 24, 200])
+def test_tc_long_items_wrap_the_ring(split):
+    """Items of many stages (the ring wraps inside an item; PV lags S by two stages),
+    lazy O rescaling across stages (peaky), and both softmax warpgroups' merge."""
+    G = workloads.Group
+    rec = workloads.Recipe("long_items", workloads.Model("m", 1, 20, 4, 128),
+                           [G(2100, 3, [18]), G(1333, None, [16, 21]), G(700, 0, [17])], seed=31)
+    lens = _lengths(rec)
+    nq = [min(16, n) for n in lens]
+    for fam in ("peaky", "needle_shared_pos"):
+        errs, _, plan = run_extend(rec, fam, nq, max_rows=128, split_pages=split, num_ctas=8)
+        _ok(errs)
