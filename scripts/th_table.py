@@ -1,0 +1,108 @@
+"""Measured attention share of the paper's hybrid-batch time T_h(P, N) on one B200 (S8(f) F3).
+
+    python scripts/th_table.py [--out profiles/r01_th_table.csv]
+
+T_h(P, N) (Table I, Eq. 3, Eq. 4) is the time of an engine step
+that decodes N requests while prefilling a set P of prompts.  Under SPAgent, a selected
+speculative request forks its agent's context c_i and prefills its L_s-token prompt over
+it ("prefill overhead is added once per speculative request, since all samples of
+one request share the same prefix").  This script measures the attention part of that
+step on this library: N agents decode one token each (contexts 2k-8k, Qwen2.5-32B shape)
+while |S| of them have a fork prefilling L_s tokens over the agent's shared pages, one
+spa_extend_plan + 64 PDL-chained layer calls (8 resident layers rotated, each far larger
+than L2).  Rows are written with the header SPEC.md's cost model reads
+(`prefill_len,prefill_count,decode_count,seconds`), seconds = attention time of one
+64-layer step.
+"""
+import argparse
+import csv
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
+from paper_2511_20048_b200 import spa  # noqa: E402
+from spa_inputs import KIND_Q, kv_bits_torch, workloads  # noqa: E402
+
+
+def recipe(n_dec, n_spec, l_s, seed):
+    rng = np.random.default_rng(seed)
+    groups = []
+    for a in range(n_dec):
+        p = int(rng.integers(2048, 8193))
+        groups.append(workloads.Group(p, int(rng.integers(0, 257)), [l_s] if a < n_spec else []))
+    return workloads.Recipe(f"th_{n_dec}_{n_spec}_{l_s}", workloads.QWEN25_32B, groups, seed=seed)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_th_table.csv"))
+    ap.add_argument("--decode", default="1,4,16,64,256")
+    ap.add_argument("--spec", default="0,1,4,16")
+    ap.add_argument("--ls", default="16,128,512")
+    ap.add_argument("--layers", type=int, default=8)
+    ap.add_argument("--calls", type=int, default=64)
+    ap.add_argument("--reps", type=int, default=3)
+    a = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    m = workloads.QWEN25_32B
+    Lr = a.layers
+    rows_out = []
+    decs = [int(x) for x in a.decode.split(",")]
+    specs = [int(x) for x in a.spec.split(",")]
+    lss = [int(x) for x in a.ls.split(",")]
+    biggest = recipe(max(decs), min(max(specs), max(decs)), max(lss), 7)
+    pool = spa.Pool(Lr, m.num_q_heads, m.num_kv_heads, m.head_dim, bench.pages_for(biggest, 40), device=dev)
+    for nd in decs:
+        for ns in specs:
+            if ns > nd:
+                continue
+            for ls in (lss if ns else [0]):
+                rec = recipe(nd, ns, max(ls, 1), 1000 + nd * 31 + ns * 7 + ls)
+                ids, reqs, batch = bench.build_batch(spa, pool, rec, list(range(Lr)), slice(0, m.num_kv_heads), dev,
+                                                     fill="reuse")
+                nq = [1 if who == "main" else ls for (gi, who) in batch]
+                rows = int(sum(nq))
+                q = kv_bits_torch(rec.seed, KIND_Q, 1, list(range(Lr)), np.arange(rows), m.num_q_heads, m.head_dim,
+                                  dev).contiguous()
+                o = torch.empty((Lr, rows, m.num_q_heads, m.head_dim), dtype=torch.bfloat16, device=dev)
+                plan = spa.Plan(pool, max_rows=128 if ns else 16)
+                plan.plan(reqs, 0, stream=stream, n_query=nq if ns else None)
+
+                def run(n):
+                    for i in range(n):
+                        plan.decode(i % Lr, q[i % Lr], o[i % Lr], None, scale=m.softmax_scale, stream=stream,
+                                    want_lse=False)
+
+                run(8)
+                torch.cuda.synchronize()
+                ts = []
+                for _ in range(a.reps):
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    run(a.calls)
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    ts.append(e0.elapsed_time(e1) / a.calls)
+                layer_ms = float(np.median(ts))
+                step_s = layer_ms * 1e-3 * m.num_layers
+                rows_out.append((ls, ns, nd, step_s))
+                print(f"decode {nd:4d}  spec {ns:3d} x {ls:4d} tokens  rows {rows:5d}  layer {layer_ms * 1e3:8.1f} us  "
+                      f"step {step_s * 1e3:7.2f} ms", flush=True)
+                for nm in ids.values():
+                    pool.free(nm)
+    with open(a.out, "w", newline="") as f:
+        w = csv.writer(f)
+        w.writerow(["prefill_len", "prefill_count", "decode_count", "seconds"])
+        for r in rows_out:
+            w.writerow([r[0], r[1], r[2], f"{r[3]:.6e}"])
+
+
+if __name__ == "__main__":
+    main()
