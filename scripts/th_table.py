@@ -8,9 +8,11 @@ speculative request forks its agent's context c_i and prefills its L_s-token pro
 it ("prefill overhead is added once per speculative request, since all samples of
 one request share the same prefix").  This script measures the attention part of that
 step on this library: N agents decode one token each (contexts 2k-8k, Qwen2.5-32B shape)
-while |S| of them have a fork prefilling L_s tokens over the agent's shared pages, one
-spa_extend_plan + 64 PDL-chained layer calls (8 resident layers rotated, each far larger
-than L2).  Rows are written with the header SPEC.md's cost model reads
+while |S| of them have a fork prefilling L_s tokens over the agent's shared pages.  One
+layer = the agents with a prefilling fork as 128-row groups on the tcgen05 extend kernel
+(parent decode row + fork prompt rows read c_i once) + the other agents on the decode
+kernel; 64 PDL-chained layer calls (8 resident layers rotated, each far larger than L2).
+Rows are written with the header SPEC.md's cost model reads
 (`prefill_len,prefill_count,decode_count,seconds`), seconds = attention time of one
 64-layer step.
 """
@@ -68,17 +70,31 @@ def main():
                 ids, reqs, batch = bench.build_batch(spa, pool, rec, list(range(Lr)), slice(0, m.num_kv_heads), dev,
                                                      fill="reuse")
                 nq = [1 if who == "main" else ls for (gi, who) in batch]
+                # the engine's composition: agents with a prefilling fork run as 128-row groups on
+                # the tcgen05 extend kernel (parent + fork read c_i once); the other agents' decode
+                # rows run on the decode kernel (a second launch per layer on the same stream)
+                spec_groups = {gi for (gi, who) in batch if who != "main"}
+                sel_x = [i for i, (gi, who) in enumerate(batch) if gi in spec_groups]
+                sel_d = [i for i, (gi, who) in enumerate(batch) if gi not in spec_groups]
+                launches = []
+                for sel, ext in ((sel_x, True), (sel_d, False)):
+                    if not sel:
+                        continue
+                    r_nq = [nq[i] for i in sel]
+                    nrows = int(sum(r_nq))
+                    qq = kv_bits_torch(rec.seed, KIND_Q, 1 + ext, list(range(Lr)), np.arange(nrows), m.num_q_heads,
+                                       m.head_dim, dev).contiguous()
+                    oo = torch.empty((Lr, nrows, m.num_q_heads, m.head_dim), dtype=torch.bfloat16, device=dev)
+                    pl = spa.Plan(pool, max_rows=128 if ext else 16)
+                    pl.plan([reqs[i] for i in sel], 0, stream=stream, n_query=r_nq if ext else None)
+                    launches.append((pl, qq, oo))
                 rows = int(sum(nq))
-                q = kv_bits_torch(rec.seed, KIND_Q, 1, list(range(Lr)), np.arange(rows), m.num_q_heads, m.head_dim,
-                                  dev).contiguous()
-                o = torch.empty((Lr, rows, m.num_q_heads, m.head_dim), dtype=torch.bfloat16, device=dev)
-                plan = spa.Plan(pool, max_rows=128 if ns else 16)
-                plan.plan(reqs, 0, stream=stream, n_query=nq if ns else None)
 
                 def run(n):
                     for i in range(n):
-                        plan.decode(i % Lr, q[i % Lr], o[i % Lr], None, scale=m.softmax_scale, stream=stream,
-                                    want_lse=False)
+                        for pl, qq, oo in launches:
+                            pl.decode(i % Lr, qq[i % Lr], oo[i % Lr], None, scale=m.softmax_scale, stream=stream,
+                                      want_lse=False)
 
                 run(8)
                 torch.cuda.synchronize()
