@@ -55,6 +55,7 @@ typedef int64_t spa_req;                 /* request id: 1, 2, 3, ... never reuse
 typedef struct spa_pool spa_pool;
 typedef struct spa_plan spa_plan;
 typedef struct spa_comm spa_comm;
+typedef struct spa_peer spa_peer;
 
 /* ---------------------------------------------------------------------------------
  * Paged KV pool
@@ -216,6 +217,46 @@ spa_status spa_comm_destroy(spa_comm* comm);
 spa_status spa_decode_attention_sharded(const spa_plan* plan, spa_comm* comm, int32_t layer,
                                         const void* q_local, int64_t q_stride_req, int64_t q_stride_head,
                                         void* o_gathered, float* lse_gathered, float scale, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * F1: fused decode + all-gather over NVLink peer memory.
+ * The decode kernel (a5, with its in-kernel split merge a6) stores every output element
+ * of this rank's heads straight into the same offset of EVERY rank's gathered buffer
+ * (peer stores through CUDA IPC mappings), and the last CTA to finish releases a flag
+ * into each peer's signal pad and waits for theirs -- the all-gather (a7) without an
+ * NCCL launch, its transfer overlapping the kernel's math item by item.  The paper's
+ * engine shards attention by tensor parallelism over NVLink GPUs.
+ *
+ * Memory: spa_peer_create allocates ONE device region per rank (library-owned, freed by
+ * spa_peer_destroy): n_bufs buffers of buf_bytes (256-B aligned) + a signal pad.  Buffer
+ * b of every rank holds, for a decode over N requests with Hq_local = Hq / world heads:
+ *     O   bf16 [world][Hq_local][N][d]   at offset 0          (= [Hq][N][d], head-major)
+ *     LSE fp32 [world][Hq_local][N]      at offset align256(world Hq_local N d 2)
+ * Wiring: spa_peer_ipc_handle exports the region (64 bytes); the caller all-gathers the
+ * handles (rank order) and passes them to spa_peer_connect, which opens the others.
+ * spa_peer_connect_local wires `world` peers created in ONE process on ONE device
+ * (virtual ranks: tests of the protocol on a single GPU; they must run on different
+ * streams, since each rank's launch waits for the others').
+ * Ordering contract: every rank makes the same sequence of fused calls (the epoch of a
+ * call is its index in that sequence).  A peer may write buffer b of call k+1 as soon as
+ * this rank's call k has completed, so consecutive calls must alternate between >= 2
+ * buffers if the caller still reads buffer b after call k (a model's O projection does).
+ * Only decode plans (max_rows <= 64) with merge_mode 0 or 1 are supported
+ * (SPA_ERR_UNSUPPORTED otherwise).  If a peer does not arrive within 20 s the kernel
+ * gives up, and spa_peer_status reports 1 (0 = healthy). */
+spa_status spa_peer_create(int32_t rank, int32_t world, size_t buf_bytes, int32_t n_bufs, spa_peer** out);
+spa_status spa_peer_ipc_handle(const spa_peer* peer, void* out_handle /* 64 bytes */);
+spa_status spa_peer_connect(spa_peer* peer, const void* handles /* world x 64 bytes, rank order */);
+spa_status spa_peer_connect_local(spa_peer* const* peers, int32_t world);
+spa_status spa_peer_buffer(const spa_peer* peer, int32_t buf_idx, void** out_ptr);
+spa_status spa_peer_status(const spa_peer* peer, int32_t* out_status);   /* synchronises the device */
+spa_status spa_peer_destroy(spa_peer* peer);
+/* Decode this rank's heads into buffer buf_idx of every rank (O, and LSE if with_lse),
+ * then meet the peers.  On return (stream-ordered) buffer buf_idx of this rank holds the
+ * gathered O / LSE of all ranks.  q_local: bf16 [N][Hq_local][d] with the given strides. */
+spa_status spa_decode_attention_fused_gather(const spa_plan* plan, spa_peer* peer, int32_t layer,
+                                             const void* q_local, int64_t q_stride_req, int64_t q_stride_head,
+                                             int32_t buf_idx, int32_t with_lse, float scale, void* stream);
 
 /* Library info */
 int32_t spa_abi_version(void);

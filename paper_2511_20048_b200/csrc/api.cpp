@@ -1,4 +1,5 @@
-// C ABI entry points of the decode step (a5/a6) and the head-sharded launcher (a7).
+// C ABI entry points of the decode step (a5/a6), the head-sharded launcher (a7) and the
+// fused decode + peer-memory all-gather (S8(f) F1).
 #include <cmath>
 #include <cstdint>
 #include <string>
@@ -9,6 +10,7 @@ namespace spa {
 // comm.cpp
 int comm_all_gather(spa_comm* comm, const void* send, void* recv, size_t count, int is_bf16, void* stream,
                     std::string* err);
+void peer_launch(spa_peer* peer, PeerLaunch* pl);
 }  // namespace spa
 
 using namespace spa;
@@ -83,6 +85,34 @@ spa_status spa_decode_attention_sharded(const spa_plan* plan, spa_comm* comm, in
         if (lse_gathered && comm_all_gather(comm, lmine, lse_gathered, size_t(Hl * N), 0, stream, &why))
             return fail(SPA_ERR_NCCL, why);
     }
+    return SPA_OK;
+}
+
+spa_status spa_decode_attention_fused_gather(const spa_plan* plan, spa_peer* peer, int32_t layer, const void* q_local,
+                                             int64_t q_stride_req, int64_t q_stride_head, int32_t buf_idx,
+                                             int32_t with_lse, float scale, void* stream) {
+    if (!peer) return fail(SPA_ERR_INVALID_ARG, "null peer");
+    if (!plan) return fail(SPA_ERR_INVALID_ARG, "null plan");
+    if (!peer->connected) return fail(SPA_ERR_INVALID_ARG, "peer not connected (spa_peer_connect)");
+    if (buf_idx < 0 || buf_idx >= peer->n_bufs) return fail(SPA_ERR_INVALID_ARG, "buffer index out of range");
+    if (plan->mt == 8 || plan->cfg.merge_mode == 2)
+        return fail(SPA_ERR_UNSUPPORTED, "fused gather needs a decode plan (max_rows <= 64) with merge_mode 0 or 1");
+    const auto& c = plan->pool->cfg;
+    const int64_t N = plan->n_req, Hl = c.num_q_heads, D = c.head_dim, W = peer->world;
+    const size_t o_bytes = size_t(W * Hl * N * D) * 2;
+    const size_t lse_off = (o_bytes + 255) & ~size_t(255);
+    if ((with_lse ? lse_off + size_t(W * Hl * N) * 4 : o_bytes) > peer->buf_bytes)
+        return fail(SPA_ERR_INVALID_ARG, "peer buffer too small for [world][Hq_local][N][d] (+ LSE)");
+    char* buf = peer->base + size_t(buf_idx) * peer->buf_stride;
+    uint16_t* mine = reinterpret_cast<uint16_t*>(buf) + size_t(peer->rank * Hl * N * D);
+    float* lmine = with_lse ? reinterpret_cast<float*>(buf + lse_off) + size_t(peer->rank * Hl * N) : nullptr;
+    if (spa_status s = check_decode_args(plan, layer, q_local, q_stride_req, q_stride_head, mine, D, N * D, scale))
+        return s;
+    PeerLaunch pl;
+    peer_launch(peer, &pl);
+    int err = launch_decode(plan, layer, q_local, q_stride_req, q_stride_head, mine, D, N * D, lmine, 1, N, scale,
+                            stream, W > 1 ? &pl : nullptr);
+    if (err) return fail(SPA_ERR_CUDA, std::string("decode kernel (fused gather): ") + cuda_error_string(err));
     return SPA_OK;
 }
 

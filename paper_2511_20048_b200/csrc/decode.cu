@@ -40,6 +40,14 @@ struct DecodeParams {
     unsigned long long* trace;   // spa_debug_set_trace timeline (null: off)
     int trace_cap;
     unsigned poll_min, poll_max;   // tail-merge polling backoff (ns)
+    // F1 fused all-gather (fan.n = world > 1): outputs also go to every peer's gathered
+    // buffer; the last CTA to finish signals the peers and waits for theirs
+    OutFan fan;
+    int rank;
+    unsigned epoch;
+    unsigned* sig_local;               // this rank's signal pad: [world] u32, written by peers
+    unsigned* sig_peer[kMaxPeers];     // peer k's signal pad as mapped here
+    unsigned* status;                  // set to 1 if the peer wait timed out
 };
 
 // A popped work item as the producer hands it to its team (shared memory): the item and
@@ -90,7 +98,7 @@ struct DecodeCfg {
 template <int D, int MT, int PPS, int TEAMS>
 __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
     decode_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
-                  const DecodeParams p) {
+                  const __grid_constant__ DecodeParams p) {
     using C = DecodeCfg<D, MT, PPS, TEAMS>;
     constexpr int KW = C::KW;
     constexpr int JW = PPS / KW;   // pages per warp per stage
@@ -161,6 +169,7 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
     int32_t* sched = const_cast<int32_t*>(meta) + meta[H_OFF_SCHED] + kSchedStride * (p.launch % kSchedSlots);
     const int n_items = meta[H_N_ITEMS];
     const int G = p.group_size, Hq = p.num_q_heads, Hkv = p.num_kv_heads;
+    const OutFan* fan = p.fan.n > 1 ? &p.fan : nullptr;
     uint64_t policy = 0;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
 
@@ -555,9 +564,8 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
                         __nv_bfloat16* orow = p.o + m.row * p.o_sr + head * p.o_sh + wk * (D / 2);
 #pragma unroll
                         for (int n = 0; n < NTH; ++n)
-                            *reinterpret_cast<__nv_bfloat162*>(orow + n * 8 + c0) =
-                                __floats2bfloat162_rn(half[n][2 * rr] * inv, half[n][2 * rr + 1] * inv);
-                        if ((lane & 3) == 0 && wk == 0 && p.lse) p.lse[m.row * p.l_sr + head * p.l_sh] = lse;
+                            st_out2(fan, orow + n * 8 + c0, half[n][2 * rr] * inv, half[n][2 * rr + 1] * inv);
+                        if ((lane & 3) == 0 && wk == 0 && p.lse) st_out1(fan, p.lse + m.row * p.l_sr + head * p.l_sh, lse);
                     } else {
                         float* prow = p.part_o + ((long long)m.rec * Hq + head) * D + wk * (D / 2);
 #pragma unroll
@@ -609,7 +617,7 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
                 float* lrow = p.lse ? p.lse + mm.row * p.l_sr : nullptr;
                 for (int hh = tw; hh < G; hh += C::TEAM_WARPS)
                     warp_merge_head<D>(p.part_o, p.part_lse, Hq, s0, s1, itm.kv_head * G + hh, orow, p.o_sh, lrow,
-                                       p.l_sh, lane);
+                                       p.l_sh, lane, D, fan);
             }
         }
     }
@@ -642,9 +650,11 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
             __nv_bfloat16* orow = p.o + row * p.o_sr;
             float* lrow = p.lse ? p.lse + row * p.l_sr : nullptr;
             if (sub == 0)
-                warp_merge_group<D>(p.part_o, p.part_lse, Hq, s0, s1, g * G, G, orow, p.o_sh, lrow, p.l_sh, lane);
+                warp_merge_group<D>(p.part_o, p.part_lse, Hq, s0, s1, g * G, G, orow, p.o_sh, lrow, p.l_sh, lane, D,
+                                    fan);
             else
-                warp_merge_head<D>(p.part_o, p.part_lse, Hq, s0, s1, g * G + sub - 1, orow, p.o_sh, lrow, p.l_sh, lane);
+                warp_merge_head<D>(p.part_o, p.part_lse, Hq, s0, s1, g * G + sub - 1, orow, p.o_sh, lrow, p.l_sh, lane,
+                                   D, fan);
             tr(5, t);
         }
     }
@@ -652,11 +662,34 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
     // the last CTA to finish rewinds the queues for the next launch (stream-ordered)
     __syncthreads();
     if (threadIdx.x == 0) {
+        // fused all-gather: this CTA's peer stores (ordered before by bar.sync) are made
+        // visible system-wide before its arrival on the CTA counter (release pattern)
+        if (fan) __threadfence_system();
         if (atomicAdd(sched + 1, 1) == int(gridDim.x) - 1) {
             sched[0] = 0;
             sched[1] = 0;
             sched[32] = 0;
             st_release_gpu(sched + 3, p.launch + kSchedSlots);   // hand the slot on
+            if (fan) {
+                // every CTA of this rank has arrived (acquire pattern), so all of this rank's
+                // output stores precede the flags; then wait for every peer's flag of this epoch
+                __threadfence_system();
+                for (int k = 0; k < p.fan.n; ++k)
+                    if (k != p.rank) st_release_sys(p.sig_peer[k] + p.rank, p.epoch);
+                unsigned long long t0, t;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+                for (int k = 0; k < p.fan.n; ++k) {
+                    if (k == p.rank) continue;
+                    while (int(ld_acquire_sys(p.sig_local + k) - p.epoch) < 0) {
+                        __nanosleep(256);
+                        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                        if (t - t0 > 20000000000ull) {   // 20 s: a peer never arrived; report, do not hang
+                            *p.status = 1u;
+                            break;
+                        }
+                    }
+                }
+            }
         }
     }
 }
@@ -695,7 +728,9 @@ bool decode_teams_supported(int mt, int teams) {
 }
 
 int launch_decode(const spa_plan* P, int32_t layer, const void* q, int64_t q_sr, int64_t q_sh, void* o, int64_t o_sr,
-                  int64_t o_sh, float* lse, int64_t l_sr, int64_t l_sh, float scale, void* stream) {
+                  int64_t o_sh, float* lse, int64_t l_sr, int64_t l_sh, float scale, void* stream,
+                  const PeerLaunch* peer) {
+    if (peer && (P->mt == 8 || P->cfg.merge_mode == 2)) return int(cudaErrorNotSupported);
     if (P->mt == 8)   // 128-row items: the tcgen05 extend kernel (ext.cu)
         return launch_ext(P, layer, q, q_sr, q_sh, o, o_sr, o_sh, lse, l_sr, l_sh, scale, stream);
     const auto& c = P->pool->cfg;
@@ -727,6 +762,17 @@ int launch_decode(const spa_plan* P, int32_t layer, const void* q, int64_t q_sr,
     static const unsigned poll_max = std::getenv("SPA_POLL_MAX") ? unsigned(std::atoi(std::getenv("SPA_POLL_MAX"))) : 256u;
     dp.poll_min = poll_min;
     dp.poll_max = poll_max;
+    if (peer && peer->world > 1) {
+        dp.fan.n = peer->world;
+        for (int k = 0; k < peer->world; ++k) {
+            dp.fan.delta[k] = peer->delta[k];
+            dp.sig_peer[k] = peer->sig_peer[k];
+        }
+        dp.rank = peer->rank;
+        dp.epoch = peer->epoch;
+        dp.sig_local = peer->sig_local;
+        dp.status = peer->status;
+    }
     int err = 0;
     err = c.head_dim == 64 ? launch_decode_d<64>(P, dp, stream) : launch_decode_d<128>(P, dp, stream);
     if (err) return err;

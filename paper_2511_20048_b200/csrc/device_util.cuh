@@ -109,6 +109,46 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// F1: output fan-out for the fused decode + all-gather.  Every
+// output element is stored at its local address and at the same offset of each peer
+// rank's gathered buffer: delta[k] is the byte distance from this rank's buffer to rank
+// k's as mapped in this process (NVLink peer memory via CUDA IPC; delta[rank] = 0).
+// fan == nullptr or n <= 1: the plain local store.
+constexpr int kMaxPeers = 8;
+struct OutFan {
+    int n;
+    int pad;
+    long long delta[kMaxPeers];
+};
+
+__device__ __forceinline__ void st_out2(const OutFan* fan, __nv_bfloat16* p, float a, float b) {
+    const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+    if (!fan || fan->n <= 1) {
+        *reinterpret_cast<__nv_bfloat162*>(p) = v;
+        return;
+    }
+    for (int k = 0; k < fan->n; ++k)
+        *reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<char*>(p) + fan->delta[k]) = v;
+}
+
+__device__ __forceinline__ void st_out1(const OutFan* fan, float* p, float v) {
+    if (!fan || fan->n <= 1) {
+        *p = v;
+        return;
+    }
+    for (int k = 0; k < fan->n; ++k) *reinterpret_cast<float*>(reinterpret_cast<char*>(p) + fan->delta[k]) = v;
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned* addr, unsigned v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(addr), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* addr) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(addr) : "memory");
+    return v;
+}
+
 // Launch with programmatic stream serialization (PDL): the kernel may start while the
 // previous kernel on the stream drains; every kernel here begins with griddepcontrol.wait
 // before touching memory the previous one wrote.  SPA_NO_PDL=1 disables it (A/B runs).
@@ -137,7 +177,8 @@ static int launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sm
 template <int DT>
 __device__ __forceinline__ void warp_merge_group_small(const float* part_o, const float* part_lse, int H, int s0, int s1,
                                                        int head0, int G, __nv_bfloat16* orow, long long o_sh,
-                                                       float* lrow, long long l_sh, int lane, int dim = DT) {
+                                                       float* lrow, long long l_sh, int lane, int dim = DT,
+                                                       const OutFan* fan = nullptr) {
     const int D = DT ? DT : dim;
     const int S = s1 - s0, GS = G * S;
     const int c = lane * 4;
@@ -176,7 +217,7 @@ __device__ __forceinline__ void warp_merge_group_small(const float* part_o, cons
             const int src = lane - hh * S;
             const float wm = __shfl_sync(0xffffffffu, w, src & 31);
             if (src >= 0 && src < S) wflat = wm;
-            if (lane == 0 && lrow) lrow[(long long)(head0 + hh) * l_sh] = lse;
+            if (lane == 0 && lrow) st_out1(fan, lrow + (long long)(head0 + hh) * l_sh, lse);
         }
     }
     float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -194,8 +235,8 @@ __device__ __forceinline__ void warp_merge_group_small(const float* part_o, cons
             if (++jj == S) {
                 if (c < D) {
                     __nv_bfloat16* op = orow + (long long)(head0 + hc) * o_sh + c;
-                    *reinterpret_cast<__nv_bfloat162*>(op) = __floats2bfloat162_rn(a.x, a.y);
-                    *reinterpret_cast<__nv_bfloat162*>(op + 2) = __floats2bfloat162_rn(a.z, a.w);
+                    st_out2(fan, op, a.x, a.y);
+                    st_out2(fan, op + 2, a.z, a.w);
                 }
                 a = make_float4(0.f, 0.f, 0.f, 0.f);
                 jj = 0;
@@ -215,7 +256,8 @@ __device__ __forceinline__ void warp_merge_group_small(const float* part_o, cons
 template <int DT>   // DT = head_dim if known at compile time, 0 = runtime `dim`
 __device__ __forceinline__ void warp_merge_head(const float* part_o, const float* part_lse, int H, int s0, int s1,
                                                 int head, __nv_bfloat16* orow, long long o_sh, float* lrow,
-                                                long long l_sh, int lane, int dim = DT) {
+                                                long long l_sh, int lane, int dim = DT,
+                                                const OutFan* fan = nullptr) {
     const int D = DT ? DT : dim;
     orow += (long long)head * o_sh;
     if (s1 - s0 <= 16 && D <= 128) {
@@ -253,10 +295,10 @@ __device__ __forceinline__ void warp_merge_head(const float* part_o, const float
             }
         }
         if (c < D) {
-            *reinterpret_cast<__nv_bfloat162*>(orow + c) = __floats2bfloat162_rn(a.x, a.y);
-            *reinterpret_cast<__nv_bfloat162*>(orow + c + 2) = __floats2bfloat162_rn(a.z, a.w);
+            st_out2(fan, orow + c, a.x, a.y);
+            st_out2(fan, orow + c + 2, a.z, a.w);
         }
-        if (lane == 0 && lrow) lrow[(long long)head * l_sh] = lse;
+        if (lane == 0 && lrow) st_out1(fan, lrow + (long long)head * l_sh, lse);
         return;
     }
     if (s1 - s0 <= 128 && D <= 128) {
@@ -302,10 +344,10 @@ __device__ __forceinline__ void warp_merge_head(const float* part_o, const float
             }
         }
         if (c < D) {
-            *reinterpret_cast<__nv_bfloat162*>(orow + c) = __floats2bfloat162_rn(a.x, a.y);
-            *reinterpret_cast<__nv_bfloat162*>(orow + c + 2) = __floats2bfloat162_rn(a.z, a.w);
+            st_out2(fan, orow + c, a.x, a.y);
+            st_out2(fan, orow + c + 2, a.z, a.w);
         }
-        if (lane == 0 && lrow) lrow[(long long)head * l_sh] = lse;
+        if (lane == 0 && lrow) st_out1(fan, lrow + (long long)head * l_sh, lse);
         return;
     }
     float m = -INFINITY;
@@ -353,11 +395,11 @@ __device__ __forceinline__ void warp_merge_head(const float* part_o, const float
             }
         }
         if (c < D) {
-            *reinterpret_cast<__nv_bfloat162*>(orow + c) = __floats2bfloat162_rn(a.x, a.y);
-            *reinterpret_cast<__nv_bfloat162*>(orow + c + 2) = __floats2bfloat162_rn(a.z, a.w);
+            st_out2(fan, orow + c, a.x, a.y);
+            st_out2(fan, orow + c + 2, a.z, a.w);
         }
     }
-    if (lane == 0 && lrow) lrow[(long long)head * l_sh] = lse;
+    if (lane == 0 && lrow) st_out1(fan, lrow + (long long)head * l_sh, lse);
 }
 
 // Merge heads [head0, head0 + G) of one request row: all G in one warp pass when
@@ -366,14 +408,15 @@ __device__ __forceinline__ void warp_merge_head(const float* part_o, const float
 template <int DT>
 __device__ __forceinline__ void warp_merge_group(const float* part_o, const float* part_lse, int H, int s0, int s1,
                                                  int head0, int G, __nv_bfloat16* orow, long long o_sh, float* lrow,
-                                                 long long l_sh, int lane, int dim = DT) {
+                                                 long long l_sh, int lane, int dim = DT,
+                                                 const OutFan* fan = nullptr) {
     const int D = DT ? DT : dim;
     if (G <= 8 && G * (s1 - s0) <= 32 && s1 - s0 <= 16 && D <= 128) {
-        warp_merge_group_small<DT>(part_o, part_lse, H, s0, s1, head0, G, orow, o_sh, lrow, l_sh, lane, dim);
+        warp_merge_group_small<DT>(part_o, part_lse, H, s0, s1, head0, G, orow, o_sh, lrow, l_sh, lane, dim, fan);
         return;
     }
     for (int hh = 0; hh < G; ++hh)
-        warp_merge_head<DT>(part_o, part_lse, H, s0, s1, head0 + hh, orow, o_sh, lrow, l_sh, lane, dim);
+        warp_merge_head<DT>(part_o, part_lse, H, s0, s1, head0 + hh, orow, o_sh, lrow, l_sh, lane, dim, fan);
 }
 
 }  // namespace spa

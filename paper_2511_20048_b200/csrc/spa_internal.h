@@ -132,13 +132,36 @@ struct spa_comm {
     int rank = 0, world = 1;
 };
 
+// F1 fused decode + all-gather (comm.cpp): one device allocation per rank holding n_bufs
+// gathered-output buffers and a signal pad, shared with the other ranks over CUDA IPC.
+struct spa_peer {
+    int rank = 0, world = 1, device = 0;
+    size_t buf_bytes = 0, buf_stride = 0;
+    int n_bufs = 0;
+    char* base = nullptr;                 // this rank's allocation (cudaMalloc)
+    size_t sig_off = 0;                   // signal pad: u32[world] at base + sig_off, then the status word
+    char* peer_base[8] = {};              // each rank's allocation as mapped in this process
+    bool ipc_opened[8] = {};
+    bool connected = false;
+    uint32_t epoch = 0;                   // fused launches so far (identical on every rank)
+};
+
 namespace spa {
 // kernels.cu launchers (all return cudaError_t as int)
 int launch_append(const spa_pool* pool, const void* k_new, const void* v_new, int32_t T_total,
                   const std::vector<int32_t>& dst_slots, void* stream);
 int launch_cow(const spa_pool* pool, int32_t src_page, int32_t dst_page, int32_t rows, void* stream);
+struct PeerLaunch {   // F1: what the decode kernel needs to fan its outputs out and meet its peers
+    int rank, world;
+    long long delta[8];   // byte distance from this rank's output buffer to rank k's (mapped here)
+    unsigned* sig_local;
+    unsigned* sig_peer[8];
+    unsigned epoch;
+    unsigned* status;
+};
 int launch_decode(const spa_plan* plan, int32_t layer, const void* q, int64_t q_sr, int64_t q_sh, void* o,
-                  int64_t o_sr, int64_t o_sh, float* lse, int64_t l_sr, int64_t l_sh, float scale, void* stream);
+                  int64_t o_sr, int64_t o_sh, float* lse, int64_t l_sr, int64_t l_sh, float scale, void* stream,
+                  const PeerLaunch* peer = nullptr);
 int launch_merge(int32_t n_req, int32_t num_heads, int32_t head_dim, const int32_t* rec_ptr, const float* part_o,
                  const float* part_lse, void* o, int64_t o_sr, int64_t o_sh, float* lse, int64_t l_sr, int64_t l_sh,
                  int grid_hint, void* stream);

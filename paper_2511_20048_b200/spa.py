@@ -6,7 +6,7 @@ PyTorch is used only for device memory, streams and process groups (tensors are 
 to the library as raw pointers + element strides).
 
 The same names as the C ABI are exported (spa_kv_alloc, spa_kv_append, ...), plus small
-convenience classes (Pool, Plan, Comm) that own the handles.
+convenience classes (Pool, Plan, Comm, Peer) that own the handles.
 """
 from __future__ import annotations
 
@@ -74,6 +74,15 @@ _SIGS = {
     "spa_comm_destroy": (c_int32, [c_void_p]),
     "spa_decode_attention_sharded": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_int64, c_int64, c_void_p,
                                                c_void_p, c_float, c_void_p]),
+    "spa_peer_create": (c_int32, [c_int32, c_int32, ctypes.c_size_t, c_int32, ctypes.POINTER(c_void_p)]),
+    "spa_peer_ipc_handle": (c_int32, [c_void_p, c_void_p]),
+    "spa_peer_connect": (c_int32, [c_void_p, c_void_p]),
+    "spa_peer_connect_local": (c_int32, [ctypes.POINTER(c_void_p), c_int32]),
+    "spa_peer_buffer": (c_int32, [c_void_p, c_int32, ctypes.POINTER(c_void_p)]),
+    "spa_peer_status": (c_int32, [c_void_p, P_int32]),
+    "spa_peer_destroy": (c_int32, [c_void_p]),
+    "spa_decode_attention_fused_gather": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_int64, c_int64, c_int32,
+                                                    c_int32, c_float, c_void_p]),
     "spa_abi_version": (c_int32, []),
     "spa_last_error": (ctypes.c_char_p, []),
     "spa_plan_debug_array": (c_int32, [c_void_p, c_int32, ctypes.POINTER(P_int32), P_int64, P_int32]),
@@ -445,3 +454,85 @@ class Comm:
         if self.h:
             _check(lib().spa_comm_destroy(self.h))
             self.h = None
+
+
+class _DevArray:
+    """A raw device pointer as a __cuda_array_interface__ object (to view library-owned
+    memory as a torch tensor without copying)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"data": (int(ptr), False), "shape": tuple(shape), "typestr": typestr,
+                                         "version": 3, "strides": None}
+
+
+class Peer:
+    """F1 fused decode + all-gather over peer memory (include/spa.h spa_peer_*).
+
+    Owns this rank's library-allocated region (n_bufs gathered-output buffers + a signal
+    pad).  Multi-process: pass the torch.distributed group; the 64-byte CUDA IPC handles
+    are all-gathered through it.  Virtual ranks in one process: Peer.local_world()."""
+
+    def __init__(self, rank: int, world: int, buf_bytes: int, n_bufs: int = 2, group=None, connect=True):
+        h = c_void_p()
+        _check(lib().spa_peer_create(rank, world, int(buf_bytes), n_bufs, ctypes.byref(h)))
+        self.h, self.rank, self.world, self.n_bufs, self.buf_bytes = h, rank, world, n_bufs, int(buf_bytes)
+        if world > 1 and connect:
+            import torch.distributed as dist  # noqa: WPS433
+
+            mine = ctypes.create_string_buffer(64)
+            _check(lib().spa_peer_ipc_handle(self.h, mine))
+            allh = [None] * world
+            dist.all_gather_object(allh, mine.raw, group=group)
+            blob = ctypes.create_string_buffer(b"".join(allh), 64 * world)
+            _check(lib().spa_peer_connect(self.h, blob))
+
+    @staticmethod
+    def local_world(world: int, buf_bytes: int, n_bufs: int = 2) -> list["Peer"]:
+        peers = [Peer(r, world, buf_bytes, n_bufs, connect=False) for r in range(world)]
+        arr = (c_void_p * world)(*[p.h.value for p in peers])
+        _check(lib().spa_peer_connect_local(arr, world))
+        return peers
+
+    @staticmethod
+    def buffer_bytes(n_req: int, num_q_heads: int, head_dim: int, with_lse: bool = True) -> int:
+        """Bytes of one gathered buffer: O bf16 [Hq][N][d] (+ LSE fp32 [Hq][N] at a 256-B offset)."""
+        ob = num_q_heads * n_req * head_dim * 2
+        return ((ob + 255) & ~255) + (num_q_heads * n_req * 4 if with_lse else 0)
+
+    def views(self, buf_idx: int, n_req: int, num_q_heads: int, head_dim: int, device=None):
+        """(O [Hq][N][d] bf16, LSE [Hq][N] fp32) views of this rank's buffer buf_idx."""
+        import torch  # noqa: WPS433
+
+        ptr = c_void_p()
+        _check(lib().spa_peer_buffer(self.h, buf_idx, ctypes.byref(ptr)))
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        o = torch.as_tensor(_DevArray(ptr.value, (num_q_heads, n_req, head_dim), "<i2"), device=dev)
+        ob = num_q_heads * n_req * head_dim * 2
+        lse = torch.as_tensor(_DevArray(ptr.value + ((ob + 255) & ~255), (num_q_heads, n_req), "<f4"), device=dev)
+        return o.view(torch.bfloat16), lse
+
+    def status(self) -> int:
+        st = c_int32()
+        _check(lib().spa_peer_status(self.h, ctypes.byref(st)))
+        return st.value
+
+    def decode(self, plan: "Plan", layer: int, q_local, buf_idx: int, scale=None, with_lse=True, stream=None):
+        d = q_local.shape[-1]
+        if scale is None:
+            scale = d ** -0.5
+        if q_local.stride(2) != 1:
+            raise ValueError("head_dim must be contiguous")
+        _check(lib().spa_decode_attention_fused_gather(
+            plan.h, self.h, int(layer), _ptr(q_local), q_local.stride(0), q_local.stride(1), int(buf_idx),
+            int(bool(with_lse)), float(scale), _stream_ptr(stream)))
+
+    def close(self):
+        if self.h:
+            _check(lib().spa_peer_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 -- interpreter shutdown
+            pass

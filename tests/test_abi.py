@@ -55,3 +55,17 @@ def test_no_torch_types_in_header():
     text = open(os.path.join(ROOT, "include", "spa.h")).read()
     for bad in ("torch", "at::", "Tensor"):
         assert bad not in text
+
+
+def test_peer_argument_errors_without_device():
+    """F1 peer calls validate their arguments before touching a device."""
+    L = spa.lib()
+    h = ctypes.c_void_p()
+    for rank, world, nb, nbufs in ((2, 2, 64, 1), (0, 9, 64, 1), (0, 2, 0, 1), (0, 2, 64, 0), (-1, 2, 64, 1)):
+        assert L.spa_peer_create(rank, world, nb, nbufs, ctypes.byref(h)) == spa.SPA_ERR_INVALID_ARG
+        assert h.value is None
+    assert L.spa_decode_attention_fused_gather(None, None, 0, None, 0, 0, 0, 1, 1.0, None) == spa.SPA_ERR_INVALID_ARG
+    assert L.spa_peer_connect_local(None, 2) == spa.SPA_ERR_INVALID_ARG
+    assert L.spa_peer_destroy(None) == spa.SPA_OK
+    assert spa.Peer.buffer_bytes(3, 10, 128) == 7680 + 120
+    assert spa.Peer.buffer_bytes(3, 10, 128, with_lse=False) == 7680
