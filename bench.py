@@ -64,6 +64,8 @@ def parse(argv=None):
                     help="cudaProfilerStart/Stop around the timed steps only (ncu --profile-from-start off); "
                          "skips parity, e2e and the cpu baseline")
     ap.add_argument("--sharing", type=int, default=1)
+    ap.add_argument("--gather", default="fused", choices=["fused", "nccl"],
+                    help="N > 1: fused decode + peer-memory all-gather (S8(f) F1) or decode + ncclAllGather")
     ap.add_argument("--merge-mode", type=int, default=0,
                     help="split merge: 0 in-kernel tail phase, 1 in-kernel last arriver, 2 PDL-chained merge kernel")
     ap.add_argument("--split-pages", type=int, default=0, help="max pages per split (0 = auto)")
@@ -295,11 +297,20 @@ def run_spa(args):
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    # SPA_BENCH_SHARE_DEVICE=1: every rank on cuda:0 over a gloo group -- a functional check
+    # of the multi-process (fused, CUDA IPC) path on a one-GPU box; its timings time-slice
+    # the contexts and mean nothing
+    share = os.environ.get("SPA_BENCH_SHARE_DEVICE") == "1"
+    if share:
+        local = 0
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {world}"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     spa.lib()
 
     recipe = recipe_for(args.config)
@@ -332,26 +343,47 @@ def run_spa(args):
               .contiguous() for s in range(2)]
     step_v = [kv_bits_torch(recipe.seed, KIND_V, 500_000 + s, layers, np.arange(N), m.num_kv_heads, d, dev)[:, :, kv_sl]
               .contiguous() for s in range(2)]
-    if world > 1:
+    comm = peer = None
+    gather = "none (1 GPU)"
+    if world > 1 and args.gather == "fused":
+        # F1: the library's peer region holds 3C gathered buffers (the e2e leg rotates three
+        # output sets); handles are all-gathered over the process group
+        try:
+            peer = spa.Peer(rank, world, spa.Peer.buffer_bytes(N, m.num_q_heads, d), n_bufs=3 * C)
+            o_views, l_views = peer.views_all(N, m.num_q_heads, d, device=dev)
+            o_all, lse_all = o_views[:C], l_views[:C]
+            gather = "fused decode + peer-memory all-gather (CUDA IPC over NVLink)"
+        except Exception as e:  # noqa: BLE001 -- fall back to NCCL, reported in the JSON line
+            gather = f"nccl (fused setup failed: {e!r:.120})"
+            peer = None
+    if world > 1 and peer is None:
         comm_id = [spa.spa_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(comm_id, src=0)
         comm = spa.Comm(comm_id[0], rank, world)
         o_all = torch.empty((C, m.num_q_heads, N, d), dtype=torch.bfloat16, device=dev)   # gathered, head-major
         lse_all = torch.empty((C, m.num_q_heads, N), dtype=torch.float32, device=dev)
-    else:
-        comm = None
+        if not gather.startswith("nccl"):
+            gather = "decode + in-place ncclAllGather"
+    elif world == 1:
         o_all = torch.empty((C, N, hq_l, d), dtype=torch.bfloat16, device=dev)
         lse_all = torch.empty((C, N, hq_l), dtype=torch.float32, device=dev)
     plans = {w: spa.Plan(pool, sharing=bool(args.sharing), split_pages=args.split_pages, merge_mode=args.merge_mode)
              for w in windows}
     state = {"step": 0, "graph": None}
 
+    def launch(ci, qq, oo, ll):
+        r, w = sched[ci]
+        if peer is not None:   # oo / ll are views of the peer buffers: recover the buffer index
+            b = (oo.data_ptr() - o_views.data_ptr()) // (o_views.stride(0) * 2)
+            peer.decode(plans[w], r, qq[ci], buf_idx=int(b) + ci, scale=m.softmax_scale, stream=stream)
+        elif comm is None:
+            plans[w].decode(r, qq[ci], oo[ci], ll[ci], scale=m.softmax_scale, stream=stream)
+        else:
+            plans[w].decode_sharded(comm, r, qq[ci], oo[ci], ll[ci], scale=m.softmax_scale, stream=stream)
+
     def layer_loop(qq, oo, ll):
-        for ci, (r, w) in enumerate(sched):
-            if comm is None:
-                plans[w].decode(r, qq[ci], oo[ci], ll[ci], scale=m.softmax_scale, stream=stream)
-            else:
-                plans[w].decode_sharded(comm, r, qq[ci], oo[ci], ll[ci], scale=m.softmax_scale, stream=stream)
+        for ci in range(C):
+            launch(ci, qq, oo, ll)
 
     def one_step(kk, vv, qq=None, oo=None, ll=None):
         qq = q_all if qq is None else qq
@@ -377,6 +409,9 @@ def run_spa(args):
     parity = None
     one_step(step_k, step_v)
     torch.cuda.synchronize()
+    if peer is not None and peer.status() != 0:
+        print(json.dumps({"error": "fused gather: a peer did not arrive (spa_peer_status)"}))
+        sys.exit(1)
     if args.profile:
         args.no_parity = args.no_e2e = True
     if not args.no_parity and rank == 0:
@@ -388,7 +423,7 @@ def run_spa(args):
             r, w = sched[ci]
             qb = kv_bits_np(recipe.seed, KIND_Q, 1_000_000, [r], np.arange(N), m.num_q_heads, d)[0]
             O, Lo = oracle_sample(recipe, batch, rows, r, qb, steps_appended=1, window=w)
-            if comm is None:
+            if world == 1:
                 og = o_all[ci, rows].float().cpu().numpy()
                 lg = lse_all[ci, rows].cpu().numpy()
                 O, Lo = O[:, q_sl], Lo[:, q_sl]
@@ -405,7 +440,12 @@ def run_spa(args):
             sys.exit(1)
 
     _log('parity', parity)
+    # the peers' next step may write the buffers rank 0 just read on the host (fused gather)
+    barrier()
     # ---- optional CUDA graph of the layer loop (plan device buffers are stable across steps)
+    if args.graph and peer is not None:
+        # a captured fused launch would replay its epoch: the peer flags would not order calls
+        raise SystemExit("--graph is not supported with --gather fused (use --gather nccl)")
     if args.graph:
         gens = {w: p.stats()["generation"] for w, p in plans.items()}
         g = torch.cuda.CUDAGraph()
@@ -440,7 +480,7 @@ def run_spa(args):
     ms = ev0.elapsed_time(ev1) / args.steps
     _log('timed steps', ms)
     if world > 1:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms], device="cpu" if share else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
 
@@ -458,12 +498,7 @@ def run_spa(args):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             for ci in cis:
-                r = sched[ci][0]
-                if comm is None:
-                    plans[w].decode(r, q_all[ci], o_all[ci], lse_all[ci], scale=m.softmax_scale, stream=stream)
-                else:
-                    plans[w].decode_sharded(comm, r, q_all[ci], o_all[ci], lse_all[ci], scale=m.softmax_scale,
-                                            stream=stream)
+                launch(ci, q_all, o_all, lse_all)
             e1.record(stream)
             barrier()
             chained.append(e0.elapsed_time(e1) / len(cis))
@@ -471,12 +506,7 @@ def run_spa(args):
         for ci in cis[: min(len(cis), 16)]:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            r = sched[ci][0]
-            if comm is None:
-                plans[w].decode(r, q_all[ci], o_all[ci], lse_all[ci], scale=m.softmax_scale, stream=stream)
-            else:
-                plans[w].decode_sharded(comm, r, q_all[ci], o_all[ci], lse_all[ci], scale=m.softmax_scale,
-                                        stream=stream)
+            launch(ci, q_all, o_all, lse_all)
             e1.record(stream)
             barrier()
             iso.append(e0.elapsed_time(e1))
@@ -511,17 +541,24 @@ def run_spa(args):
         hq = q_all.cpu().pin_memory()
         hk = step_k[0].cpu().pin_memory()
         hv = step_v[0].cpu().pin_memory()
-        ho = [torch.empty(o_all.shape, dtype=o_all.dtype).pin_memory() for _ in range(2)]
-        hl = [torch.empty(lse_all.shape, dtype=lse_all.dtype).pin_memory() for _ in range(2)]
+        # output sets: with the fused gather a peer's step i+1 may write step i-2's set as soon as
+        # this rank finished step i, so its copy-out must be done by then (3 sets, wait on i-2)
+        nb = 3 if peer is not None else 2
+        ho = [torch.empty(o_all.shape, dtype=o_all.dtype).pin_memory() for _ in range(nb)]
+        hl = [torch.empty(lse_all.shape, dtype=lse_all.dtype).pin_memory() for _ in range(nb)]
         dq = [torch.empty_like(q_all) for _ in range(2)]
         dk = [torch.empty_like(step_k[0]) for _ in range(2)]
         dv = [torch.empty_like(step_v[0]) for _ in range(2)]
-        do = [o_all, torch.empty_like(o_all)]
-        dl = [lse_all, torch.empty_like(lse_all)]
+        if peer is not None:
+            do = [o_views[j * C:(j + 1) * C] for j in range(nb)]
+            dl = [l_views[j * C:(j + 1) * C] for j in range(nb)]
+        else:
+            do = [o_all, torch.empty_like(o_all)]
+            dl = [lse_all, torch.empty_like(lse_all)]
         cs = torch.cuda.Stream(device=dev)
         ev_in = [torch.cuda.Event() for _ in range(2)]
         ev_done = [torch.cuda.Event() for _ in range(2)]
-        ev_out = [torch.cuda.Event() for _ in range(2)]
+        ev_out = [torch.cuda.Event() for _ in range(nb)]
         e2e_steps = max(4, min(args.steps, 10))
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -541,24 +578,24 @@ def run_spa(args):
 
         stage_in(0)
         for i in range(e2e_steps):
-            b = i % 2
+            b, bo = i % 2, i % nb
             if i + 1 < e2e_steps:
                 stage_in(i + 1)
             stream.wait_event(ev_in[b])
             if i >= 2:
-                stream.wait_event(ev_out[b])        # step i-2's outputs have left buffer b
-            one_step(dk[b], dv[b], dq[b], do[b], dl[b])
+                stream.wait_event(ev_out[(i - 2) % nb])   # step i-2's outputs have been copied out
+            one_step(dk[b], dv[b], dq[b], do[bo], dl[bo])
             ev_done[b].record(stream)
             with torch.cuda.stream(cs):
                 cs.wait_event(ev_done[b])
-                ho[b].copy_(do[b], non_blocking=True)
-                hl[b].copy_(dl[b], non_blocking=True)
-                ev_out[b].record(cs)
+                ho[bo].copy_(do[bo], non_blocking=True)
+                hl[bo].copy_(dl[bo], non_blocking=True)
+                ev_out[bo].record(cs)
         e1.record(cs)
         barrier()
         e2e_ms = e0.elapsed_time(e1) / e2e_steps
         if world > 1:
-            t = torch.tensor([e2e_ms], device=dev)
+            t = torch.tensor([e2e_ms], device="cpu" if share else dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
         h2d = hq.numel() * 2 + hk.numel() * 2 * 2
@@ -567,6 +604,7 @@ def run_spa(args):
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "pipelining": "H2D/D2H on a copy stream, double-buffered"}
 
+    ws_step = sum(pw["alg_bytes"] * pw["calls"] for pw in per_window.values())   # distinct layers per call
     result = None
     if rank == 0:
         cpu = cpu_baseline(recipe, batch, args.cpu_seconds) if world == 1 and not args.profile else None
@@ -595,9 +633,10 @@ def run_spa(args):
                        "resident_layers": Lr, "windows": windows,
                        "q_heads": m.num_q_heads, "kv_heads": m.num_kv_heads, "head_dim": d,
                        "parallelism": f"kv-head sharded x{world}" if world > 1 else "1 GPU",
+                       "gather": gather,
                        "sharing": bool(args.sharing), "cuda_graph": bool(args.graph),
-                       "l2": "inputs larger than L2 (KV per layer > 126 MB), no flush"
-                       if dom["alg_bytes"] > 4 * 126e6 else "KV per layer fits L2: latency, not bandwidth"},
+                       "l2": "inputs larger than L2 (the KV a step's calls read > 4 x 126 MB, layers rotate), no flush"
+                       if ws_step > 4 * 126e6 else "KV of a step fits L2: latency, not bandwidth"},
             "gpu_launches": int(launches_per_step * args.steps),
             "layer_ms": dom["layer_ms"],
             "layer_ms_isolated": dom["layer_ms_isolated"],
@@ -625,8 +664,16 @@ def run_spa(args):
         }
         print(json.dumps(result), flush=True)
     if world > 1:
+        torch.cuda.synchronize()
         dist.barrier()
-        comm.close()
+        if comm is not None:
+            comm.close()
+        if peer is not None:
+            fail = peer.status()
+            dist.barrier()   # every rank is done with the others' buffers before any is freed
+            peer.close()
+            if fail and rank == 0:
+                print(json.dumps({"error": "fused gather: a peer did not arrive (spa_peer_status)"}), flush=True)
         dist.destroy_process_group()
     return result
 

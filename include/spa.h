@@ -238,9 +238,11 @@ spa_status spa_decode_attention_sharded(const spa_plan* plan, spa_comm* comm, in
  * (virtual ranks: tests of the protocol on a single GPU; they must run on different
  * streams, since each rank's launch waits for the others').
  * Ordering contract: every rank makes the same sequence of fused calls (the epoch of a
- * call is its index in that sequence).  A peer may write buffer b of call k+1 as soon as
- * this rank's call k has completed, so consecutive calls must alternate between >= 2
- * buffers if the caller still reads buffer b after call k (a model's O projection does).
+ * call is its index in that sequence).  Any rank's call k+1 may start writing into every
+ * rank's buffer as soon as ALL ranks have finished call k.  So a buffer that call k+1
+ * writes must no longer be read on any rank once that rank's call k is done: e.g.
+ * alternate two buffers and consume call k-1's output before issuing call k (stream
+ * order), as a model's O projection between layers does.
  * Only decode plans (max_rows <= 64) with merge_mode 0 or 1 are supported
  * (SPA_ERR_UNSUPPORTED otherwise).  If a peer does not arrive within 20 s the kernel
  * gives up, and spa_peer_status reports 1 (0 = healthy). */

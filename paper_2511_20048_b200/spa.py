@@ -511,6 +511,22 @@ class Peer:
         lse = torch.as_tensor(_DevArray(ptr.value + ((ob + 255) & ~255), (num_q_heads, n_req), "<f4"), device=dev)
         return o.view(torch.bfloat16), lse
 
+    def views_all(self, n_req: int, num_q_heads: int, head_dim: int, device=None):
+        """(O [n_bufs][Hq][N][d] bf16, LSE [n_bufs][Hq][N] fp32): every buffer at once, strided."""
+        import torch  # noqa: WPS433
+
+        ptr = c_void_p()
+        _check(lib().spa_peer_buffer(self.h, 0, ctypes.byref(ptr)))
+        stride = (self.buf_bytes + 255) & ~255
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        H, N, d = num_q_heads, n_req, head_dim
+        oa = _DevArray(ptr.value, (self.n_bufs, H, N, d), "<i2")
+        oa.__cuda_array_interface__["strides"] = (stride, N * d * 2, d * 2, 2)
+        ob = H * N * d * 2
+        la = _DevArray(ptr.value + ((ob + 255) & ~255), (self.n_bufs, H, N), "<f4")
+        la.__cuda_array_interface__["strides"] = (stride, N * 4, 4)
+        return torch.as_tensor(oa, device=dev).view(torch.bfloat16), torch.as_tensor(la, device=dev)
+
     def status(self) -> int:
         st = c_int32()
         _check(lib().spa_peer_status(self.h, ctypes.byref(st)))
