@@ -81,6 +81,24 @@ typedef struct spa_pool_config {
 spa_status spa_pool_create(const spa_pool_config* cfg, void* k_pool, void* v_pool, spa_pool** out);
 spa_status spa_pool_destroy(spa_pool* pool);
 
+/* F4: a pool of FP8 (e4m3) KV pages -- half the bytes a decode
+ * step reads.  Same paging rules and calls as spa_pool_create; head_dim must be 128.
+ *   kv_scale: caller-owned device fp32 [L][Hkv][2] = (k_scale, v_scale) per layer and KV
+ *     head, static (reading F4-a: a page of an append-only stream cannot fix its
+ *     scale before it fills).  spa_kv_append still takes bf16 K/V and quantises on the way
+ *     in:  code = e4m3 round-to-nearest-even, saturating at +-448, of fp32(x) / scale
+ *     (IEEE fp32 division; oracle/fp8.py), and decode reads K = k_scale * code,
+ *     V = v_scale * code.
+ *   k_pool: e4m3 [L][num_pages][Hkv][16][128] (token-major rows, as bf16 pools).
+ *   v_pool: e4m3 [L][num_pages][Hkv][128][16]: each (page, head) block TRANSPOSED, and
+ *     page slot s stored in column 4((s mod 8) div 2) + (s mod 2) + 2(s div 8), so the
+ *     decode kernel's f16 MMA fragments are single 4-byte loads.
+ *   Both 128-byte aligned, num_layers * num_pages * Hkv * 16 * 8 < 2^31.
+ * Decode plans over it must use max_rows <= 64 (the tcgen05 extend kernel is bf16 only:
+ * CUDA error "operation not supported" at launch otherwise). */
+spa_status spa_pool_create_fp8(const spa_pool_config* cfg, void* k_pool, void* v_pool, const float* kv_scale,
+                               spa_pool** out);
+
 /* a1: a new, empty request (length 0, no pages). */
 spa_status spa_kv_alloc(spa_pool* pool, spa_req* out_req);
 

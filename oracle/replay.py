@@ -10,6 +10,7 @@ from __future__ import annotations
 import numpy as np
 
 from .attention import decode_attention, extend_attention
+from .fp8 import dequantize_e4m3, quantize_kv
 from .kvmodel import OK, LogicalKV, PagingModel
 
 
@@ -21,11 +22,14 @@ def bits_to_f64(bits) -> np.ndarray:
 class Replay:
     """Dense logical KV (+ optional paging model) built from a call log."""
 
-    def __init__(self, inputs, num_pages: int | None = None, page_size: int = 16, names=None):
+    def __init__(self, inputs, num_pages: int | None = None, page_size: int = 16, names=None, kv_fp8_scale=None):
         """inputs: spa_inputs.families.BatchInputs.  names: restrict data to these
-        request names (and whatever they fork from) -- everything else is metadata only."""
+        request names (and whatever they fork from) -- everything else is metadata only.
+        kv_fp8_scale: [L_stored, Hkv, 2] (k_scale, v_scale) -> the pool stores e4m3 codes
+        (S8(f) F4): attention runs on scale * e4m3(fp32(x) / scale) (oracle/fp8.py)."""
         m = inputs.recipe.model
         self.inputs = inputs
+        self.fp8 = None if kv_fp8_scale is None else np.asarray(kv_fp8_scale, dtype=np.float32)
         self.kv = LogicalKV(len(inputs.layers), m.num_kv_heads, m.head_dim)
         self.paging = PagingModel(num_pages, page_size) if num_pages else None
         self.rid = {}
@@ -57,6 +61,17 @@ class Replay:
         if self.paging:
             assert self.paging.append([self.rid[n] for n in names], [1] * len(names)) == OK
 
+    def kv_f64(self, name, layer_pos: int):
+        """fp64 (K, V) [n, Hkv, d] of a request at stored-layer index layer_pos, as the pool holds them."""
+        K = bits_to_f64(self.kv.K[name][layer_pos])
+        V = bits_to_f64(self.kv.V[name][layer_pos])
+        if self.fp8 is not None:
+            ks = self.fp8[layer_pos, :, 0][None, :, None]
+            vs = self.fp8[layer_pos, :, 1][None, :, None]
+            K = dequantize_e4m3(quantize_kv(K.astype(np.float32), ks), ks)
+            V = dequantize_e4m3(quantize_kv(V.astype(np.float32), vs), vs)
+        return K, V
+
     def expected(self, layer_pos: int, q_bits, names=None, window: int = 0, scale=None):
         """fp64 (O [N, Hq, d], LSE [N, Hq]) for the batch at stored-layer index layer_pos."""
         m = self.inputs.recipe.model
@@ -65,8 +80,7 @@ class Replay:
         O = np.zeros((len(names), m.num_q_heads, m.head_dim))
         LSE = np.zeros((len(names), m.num_q_heads))
         for i, nm in enumerate(names):
-            K = bits_to_f64(self.kv.K[nm][layer_pos])
-            V = bits_to_f64(self.kv.V[nm][layer_pos])
+            K, V = self.kv_f64(nm, layer_pos)
             O[i], LSE[i] = decode_attention(bits_to_f64(q_bits[i]), K, V, scale, window)
         return O, LSE
 
@@ -82,8 +96,7 @@ class Replay:
         r0 = 0
         for i, nm in enumerate(names):
             T = int(n_query[i])
-            K = bits_to_f64(self.kv.K[nm][layer_pos])
-            V = bits_to_f64(self.kv.V[nm][layer_pos])
+            K, V = self.kv_f64(nm, layer_pos)
             O[r0:r0 + T], LSE[r0:r0 + T] = extend_attention(bits_to_f64(q_rows_bits[r0:r0 + T]), K, V, scale, window)
             r0 += T
         return O, LSE

@@ -48,6 +48,9 @@ struct DecodeParams {
     unsigned* sig_local;               // this rank's signal pad: [world] u32, written by peers
     unsigned* sig_peer[kMaxPeers];     // peer k's signal pad as mapped here
     unsigned* status;                  // set to 1 if the peer wait timed out
+    // F4 fp8 pages: (k_scale, v_scale) per (layer, KV head)
+    const float* kv_scale;
+    int layer;
 };
 
 // A popped work item as the producer hands it to its team (shared memory): the item and
@@ -63,13 +66,13 @@ constexpr int kQkChains = SPA_QK_CHAINS;   // independent HMMA accumulation chai
 
 constexpr int kSmemMax = 232448;   // 227 KB: the sm_100 per-block dynamic shared memory limit
 
-template <int D, int MT, int PPS, int TEAMS_>
+template <int D, int MT, int PPS, int TEAMS_, bool F8 = false>
 struct DecodeCfg {
     static constexpr int KW = 2;                          // key-split warps per row tile
     static constexpr int TEAM_WARPS = MT * KW;
     static constexpr int TEAMS = TEAMS_;                  // teams (independent rings) per CTA
     static constexpr int WARPS = TEAMS * TEAM_WARPS;
-    static constexpr int PAGE_BYTES = kPageSize * D * 2;  // K (or V) of one page, one head
+    static constexpr int PAGE_BYTES = kPageSize * D * (F8 ? 1 : 2);  // K (or V) of one page, one head
     static constexpr int STAGE_BYTES = PPS * 2 * PAGE_BYTES;
     // per (team, row tile): column-half exchange [2][16][D/2] fp32 + (m, l) [2][16][2]
     static constexpr int COMB_BYTES = TEAMS * MT * (2 * 16 * (D / 2) * 4 + 2 * 16 * 2 * 4);
@@ -95,11 +98,12 @@ struct DecodeCfg {
     static_assert(SMEM <= kSmemMax, "shared memory over the sm_100 limit");
 };
 
-template <int D, int MT, int PPS, int TEAMS>
-__global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
+template <int D, int MT, int PPS, int TEAMS, bool F8>
+__global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8>::WARPS * 32, 1)
     decode_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                   const __grid_constant__ DecodeParams p) {
-    using C = DecodeCfg<D, MT, PPS, TEAMS>;
+    using C = DecodeCfg<D, MT, PPS, TEAMS, F8>;
+    static_assert(!F8 || D == 128, "fp8 pages: d = 128");
     constexpr int KW = C::KW;
     constexpr int JW = PPS / KW;   // pages per warp per stage
     constexpr int KS = D / 16;     // k16 steps over the head dimension
@@ -244,7 +248,9 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
             for (int j = 0; j < PPS; ++j) {
                 if (j < npg) {
                     tma_load_3d(sb + j * 2 * C::PAGE_BYTES, &tmk, 0, row[j], 0, fb, policy);
-                    tma_load_3d(sb + j * 2 * C::PAGE_BYTES + C::PAGE_BYTES, &tmv, 0, row[j], 0, fb, policy);
+                    // fp8: V^T rows are d channels of a page-head, D of them per page-head
+                    tma_load_3d(sb + j * 2 * C::PAGE_BYTES + C::PAGE_BYTES, &tmv, 0, F8 ? row[j] * (D / 16) : row[j],
+                                0, fb, policy);
                 }
             }
         }
@@ -314,17 +320,23 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
                 hi1 = m.hi;
                 q1 = p.q + m.row * p.q_sr + (itm.kv_head * G + row1 - mb * G) * p.q_sh;
             }
-            const int cq = 2 * (lane & 3);
+            // fp8: the MMA's k index 2t+i (+8) reads channel 4t+i (+2) of each 16-channel block
+            // -- the same permutation as the K fragment, so q.k is unchanged -- in f16
+            const int cq = F8 ? 4 * (lane & 3) : 2 * (lane & 3);
+            const int c2 = F8 ? 2 : 8;
 #pragma unroll
             for (int ks = 0; ks < KS; ++ks) {
                 if (q0) {
                     qa[ks][0] = *reinterpret_cast<const uint32_t*>(q0 + ks * 16 + cq);
-                    qa[ks][2] = *reinterpret_cast<const uint32_t*>(q0 + ks * 16 + cq + 8);
+                    qa[ks][2] = *reinterpret_cast<const uint32_t*>(q0 + ks * 16 + cq + c2);
                 }
                 if (q1) {
                     qa[ks][1] = *reinterpret_cast<const uint32_t*>(q1 + ks * 16 + cq);
-                    qa[ks][3] = *reinterpret_cast<const uint32_t*>(q1 + ks * 16 + cq + 8);
+                    qa[ks][3] = *reinterpret_cast<const uint32_t*>(q1 + ks * 16 + cq + c2);
                 }
+                if (F8)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) qa[ks][e] = bf16x2_to_f16x2(qa[ks][e]);
             }
         }
         // keys in [lo_warp, hi_warp) are live for every row of the warp: such pages need no mask
@@ -335,6 +347,11 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
             hi_warp = min(hi_warp, __shfl_xor_sync(0xffffffffu, hi_warp, o));
         }
         hi_warp = min(hi_warp, dsc.tok_end);
+        float scale_l2 = p.scale_log2, v_scale = 1.f;
+        if (F8) {   // K = k_scale * code folds into the logit scale, V = v_scale * code into 1/l
+            scale_l2 *= __ldg(p.kv_scale + (p.layer * Hkv + itm.kv_head) * 2);
+            v_scale = __ldg(p.kv_scale + (p.layer * Hkv + itm.kv_head) * 2 + 1);
+        }
         // running max per row, log2 units, raised lazily (only when a page's max exceeds it
         // by > kRescale, so P <= 2^kRescale); the same m is used for P, l and the LSE.
         constexpr float kRescale = 8.f;
@@ -366,15 +383,29 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
                         for (int ch = 0; ch < kQkChains; ++ch)
 #pragma unroll
                             for (int e = 0; e < 4; ++e) sc[ch][0][e] = sc[ch][1][e] = 0.f;
+                        if constexpr (F8) {
+                            // K rows of 128 e4m3 bytes, 128-B swizzled: key row nt*8 + g, channels
+                            // 4t..4t+3 of 16-B chunk ks -> the f16 B fragment (k 2t, 2t+1, 2t+8, 2t+9)
 #pragma unroll
-                        for (int ks = 0; ks < KS; ++ks) {
-                            const int dcol = ks * 16 + ((lane >> 3) & 1) * 8;
-                            const uint32_t addr =
-                                kb + (dcol >> 6) * 2048 + key * 128 + ((((dcol & 63) >> 3) ^ (key & 7)) << 4);
-                            uint32_t b0, b1, b2, b3;
-                            ldsm_x4(b0, b1, b2, b3, addr);
-                            mma16816(sc[ks % kQkChains][0], qa[ks], b0, b1);
-                            mma16816(sc[ks % kQkChains][1], qa[ks], b2, b3);
+                            for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+                                for (int nt = 0; nt < 2; ++nt) {
+                                    const int kr = nt * 8 + (lane >> 2);
+                                    const uint32_t w = lds32(kb + kr * 128 + (((ks ^ kr) & 7) << 4) + 4 * (lane & 3));
+                                    mma16816_f16(sc[ks % kQkChains][nt], qa[ks], e4m3x2_to_f16x2(w),
+                                                 e4m3x2_to_f16x2(w >> 16));
+                                }
+                        } else {
+#pragma unroll
+                            for (int ks = 0; ks < KS; ++ks) {
+                                const int dcol = ks * 16 + ((lane >> 3) & 1) * 8;
+                                const uint32_t addr =
+                                    kb + (dcol >> 6) * 2048 + key * 128 + ((((dcol & 63) >> 3) ^ (key & 7)) << 4);
+                                uint32_t b0, b1, b2, b3;
+                                ldsm_x4(b0, b1, b2, b3, addr);
+                                mma16816(sc[ks % kQkChains][0], qa[ks], b0, b1);
+                                mma16816(sc[ks % kQkChains][1], qa[ks], b2, b3);
+                            }
                         }
 #pragma unroll
                         for (int nt = 0; nt < 2; ++nt)
@@ -399,7 +430,7 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
                         for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
                             for (int e = 0; e < 4; ++e) {
-                                const float v = s[jj][nt][e] * p.scale_log2;
+                                const float v = s[jj][nt][e] * scale_l2;
                                 s[jj][nt][e] = v;
                                 if (e < 2) mx0 = fmaxf(mx0, v);
                                 else mx1 = fmaxf(mx1, v);
@@ -413,7 +444,7 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
                                 const int lo = (e < 2) ? lo0 : lo1;
                                 const int hi = (e < 2) ? hi0 : hi1;
                                 const bool ok = (j < npg) && (tok < dsc.tok_end) && (tok >= lo) && (tok < hi);
-                                const float v = ok ? s[jj][nt][e] * p.scale_log2 : -INFINITY;
+                                const float v = ok ? s[jj][nt][e] * scale_l2 : -INFINITY;
                                 s[jj][nt][e] = v;
                                 if (e < 2) mx0 = fmaxf(mx0, v);
                                 else mx1 = fmaxf(mx1, v);
@@ -462,20 +493,38 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
                             l1 += e[nt][2] + e[nt][3];
                         }
                         uint32_t pa[4];
-                        pa[0] = pack_bf16(e[0][0], e[0][1]);
-                        pa[1] = pack_bf16(e[0][2], e[0][3]);
-                        pa[2] = pack_bf16(e[1][0], e[1][1]);
-                        pa[3] = pack_bf16(e[1][2], e[1][3]);
+                        if constexpr (F8) {   // P <= 2^8 (lazy rescale): f16 holds it with 11 bits
+                            pa[0] = pack_f16(e[0][0], e[0][1]);
+                            pa[1] = pack_f16(e[0][2], e[0][3]);
+                            pa[2] = pack_f16(e[1][0], e[1][1]);
+                            pa[3] = pack_f16(e[1][2], e[1][3]);
+                        } else {
+                            pa[0] = pack_bf16(e[0][0], e[0][1]);
+                            pa[1] = pack_bf16(e[0][2], e[0][3]);
+                            pa[2] = pack_bf16(e[1][0], e[1][1]);
+                            pa[3] = pack_bf16(e[1][2], e[1][3]);
+                        }
                         const uint32_t vb = sb + j * 2 * C::PAGE_BYTES + C::PAGE_BYTES;
-                        const int key = (((lane >> 3) & 1) << 3) + (lane & 7);
+                        if constexpr (F8) {
+                            // V^T rows of 16 slot bytes (columns kF8VCol): channel n*8 + g, slots
+                            // (2t, 2t+1, 2t+8, 2t+9) at 4t..4t+3 -> the f16 B fragment of PV
 #pragma unroll
-                        for (int dn = 0; dn < KS; ++dn) {
-                            const int dchunk = 2 * dn + (lane >> 4);
-                            const uint32_t addr = vb + (dchunk >> 3) * 2048 + key * 128 + (((dchunk & 7) ^ (key & 7)) << 4);
-                            uint32_t b0, b1, b2, b3;
-                            ldsm_x4_t(b0, b1, b2, b3, addr);
-                            mma16816(acc[2 * dn], pa, b0, b1);
-                            mma16816(acc[2 * dn + 1], pa, b2, b3);
+                            for (int n = 0; n < NT; ++n) {
+                                const uint32_t w = lds32(vb + (n * 8 + (lane >> 2)) * 16 + 4 * (lane & 3));
+                                mma16816_f16(acc[n], pa, e4m3x2_to_f16x2(w), e4m3x2_to_f16x2(w >> 16));
+                            }
+                        } else {
+                            const int key = (((lane >> 3) & 1) << 3) + (lane & 7);
+#pragma unroll
+                            for (int dn = 0; dn < KS; ++dn) {
+                                const int dchunk = 2 * dn + (lane >> 4);
+                                const uint32_t addr =
+                                    vb + (dchunk >> 3) * 2048 + key * 128 + (((dchunk & 7) ^ (key & 7)) << 4);
+                                uint32_t b0, b1, b2, b3;
+                                ldsm_x4_t(b0, b1, b2, b3, addr);
+                                mma16816(acc[2 * dn], pa, b0, b1);
+                                mma16816(acc[2 * dn + 1], pa, b2, b3);
+                            }
                         }
                     }
                 }
@@ -558,7 +607,7 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
                     const int head = itm.kv_head * G + (row - mb * G);
                     const float l = rr ? lt1 : lt0;
                     const float mm = rr ? mt1 : mt0;
-                    const float inv = l > 0.f ? 1.f / l : 0.f;
+                    const float inv = l > 0.f ? v_scale / l : 0.f;
                     const float lse = l > 0.f ? (mm + log2f(l)) * 0.69314718055994531f : -INFINITY;
                     if (m.rec < 0) {
                         __nv_bfloat16* orow = p.o + m.row * p.o_sr + head * p.o_sh + wk * (D / 2);
@@ -694,20 +743,32 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS>::WARPS * 32, 1)
     }
 }
 
-template <int D, int MT, int PPS, int TEAMS>
+template <int D, int MT, int PPS, int TEAMS, bool F8 = false>
 static int launch_decode_t(const spa_plan* P, const DecodeParams& dp, void* stream) {
-    using C = DecodeCfg<D, MT, PPS, TEAMS>;
+    using C = DecodeCfg<D, MT, PPS, TEAMS, F8>;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(decode_kernel<D, MT, PPS, TEAMS>,
+        cudaError_t e = cudaFuncSetAttribute(decode_kernel<D, MT, PPS, TEAMS, F8>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
         if (e) return int(e);
         attr_set = true;
     }
     const CUtensorMap* tk = reinterpret_cast<const CUtensorMap*>(P->pool->tmap_k.bytes);
     const CUtensorMap* tv = reinterpret_cast<const CUtensorMap*>(P->pool->tmap_v.bytes);
-    return launch_pdl(decode_kernel<D, MT, PPS, TEAMS>, dim3(P->num_ctas), dim3(C::WARPS * 32), C::SMEM, stream,
+    return launch_pdl(decode_kernel<D, MT, PPS, TEAMS, F8>, dim3(P->num_ctas), dim3(C::WARPS * 32), C::SMEM, stream,
                       *tk, *tv, dp);
+}
+
+// F4 fp8 pages (d = 128): the same team shapes as bf16
+static int launch_decode_f8(const spa_plan* P, const DecodeParams& dp, void* stream) {
+    if (P->mt == 1) {
+        if (P->teams == 1) return launch_decode_t<128, 1, 2, 1, true>(P, dp, stream);
+        if (P->teams == 2) return launch_decode_t<128, 1, 2, 2, true>(P, dp, stream);
+        return launch_decode_t<128, 1, 2, 4, true>(P, dp, stream);
+    }
+    if (P->mt == 4) return launch_decode_t<128, 4, 2, 1, true>(P, dp, stream);
+    if (P->teams == 1) return launch_decode_t<128, 2, 2, 1, true>(P, dp, stream);
+    return launch_decode_t<128, 2, 2, 2, true>(P, dp, stream);
 }
 
 template <int D>
@@ -731,6 +792,7 @@ int launch_decode(const spa_plan* P, int32_t layer, const void* q, int64_t q_sr,
                   int64_t o_sh, float* lse, int64_t l_sr, int64_t l_sh, float scale, void* stream,
                   const PeerLaunch* peer) {
     if (peer && (P->mt == 8 || P->cfg.merge_mode == 2)) return int(cudaErrorNotSupported);
+    if (P->pool->kv_fp8 && P->mt == 8) return int(cudaErrorNotSupported);   // the tcgen05 extend kernel is bf16
     if (P->mt == 8)   // 128-row items: the tcgen05 extend kernel (ext.cu)
         return launch_ext(P, layer, q, q_sr, q_sh, o, o_sr, o_sh, lse, l_sr, l_sh, scale, stream);
     const auto& c = P->pool->cfg;
@@ -773,8 +835,13 @@ int launch_decode(const spa_plan* P, int32_t layer, const void* q, int64_t q_sr,
         dp.sig_local = peer->sig_local;
         dp.status = peer->status;
     }
+    dp.kv_scale = P->pool->kv_scale;
+    dp.layer = layer;
     int err = 0;
-    err = c.head_dim == 64 ? launch_decode_d<64>(P, dp, stream) : launch_decode_d<128>(P, dp, stream);
+    if (P->pool->kv_fp8)
+        err = launch_decode_f8(P, dp, stream);
+    else
+        err = c.head_dim == 64 ? launch_decode_d<64>(P, dp, stream) : launch_decode_d<128>(P, dp, stream);
     if (err) return err;
     if (H[H_N_RECORDS] > 0 && !dp.fused_merge)
         err = launch_merge(H[H_N_REQ], c.num_q_heads, c.head_dim, P->d_meta + H[H_OFF_REC_PTR], P->d_part_o,

@@ -38,7 +38,7 @@ const char* cuda_error_string(int err) { return cudaGetErrorString(cudaError_t(e
 
 static size_t pool_bytes(const spa_pool* p) {
     const auto& c = p->cfg;
-    return size_t(c.num_layers) * c.num_pages * c.num_kv_heads * c.page_size * c.head_dim * 2;
+    return size_t(c.num_layers) * c.num_pages * c.num_kv_heads * c.page_size * c.head_dim * (p->kv_fp8 ? 1 : 2);
 }
 
 int memset_pool(spa_pool* p) {
@@ -76,6 +76,29 @@ bool make_tensor_maps(spa_pool* p, std::string* err) {
     }
     const auto& c = p->cfg;
     const cuuint64_t rows = cuuint64_t(c.num_layers) * c.num_pages * c.num_kv_heads * c.page_size;
+    if (p->kv_fp8) {
+        // F4, d = 128: K rows of 128 e4m3 bytes, one (page, head) = a 128 x 16 box with
+        // 128-B swizzle; V^T rows of 16 bytes (one d channel of a page's 16 slots), one
+        // (page, head) = a 16 x 128 box, unswizzled (the kernel's 4-B loads of 8 rows x 16 B
+        // are conflict-free as laid out).  A unit third dimension keeps the 3-D TMA call.
+        const cuuint64_t vrows = rows * cuuint64_t(c.head_dim / c.page_size);
+        cuuint64_t kd[3] = {128, rows, 1}, vd[3] = {16, vrows, 1};
+        cuuint64_t ks[2] = {128, rows * 128}, vs[2] = {16, vrows * 16};
+        cuuint32_t kb[3] = {128, 16, 1}, vb[3] = {16, 128, 1};
+        cuuint32_t estr[3] = {1, 1, 1};
+        CUresult r = enc(reinterpret_cast<CUtensorMap*>(p->tmap_k.bytes), CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, p->k_pool,
+                         kd, ks, kb, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r == CUDA_SUCCESS)
+            r = enc(reinterpret_cast<CUtensorMap*>(p->tmap_v.bytes), CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, p->v_pool, vd,
+                    vs, vb, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            *err = "CUresult " + std::to_string(int(r));
+            return false;
+        }
+        return true;
+    }
     cuuint64_t dims[3] = {64, rows, cuuint64_t(c.head_dim / 64)};
     cuuint64_t strides[2] = {cuuint64_t(c.head_dim) * 2, 128};
     cuuint32_t box[3] = {64, 16, cuuint32_t(c.head_dim / 64)};
@@ -122,9 +145,81 @@ __global__ void append_kernel(const __grid_constant__ AppendParams p) {
     }
 }
 
+// F4: quantise to e4m3 on the way in (oracle/fp8.py: code = RNE_SATFINITE(fp32(x) /
+// scale), the division IEEE fp32).  One thread per (token, head, 8 channels): K's 8 codes
+// are one 8-B store into the token's row; V's go to 8 channel rows of the page's V^T block
+// at the slot's permuted column kF8VCol(slot).
+struct AppendF8Params {
+    const uint4* k_src;
+    const uint4* v_src;
+    uint8_t* k_dst;
+    uint8_t* v_dst;
+    const float* scale;      // [L][Hkv][2]
+    long long layer_stride;  // bytes: num_pages * Hkv * 16 * 128
+    int T_total, t0, n, Hkv;
+    int slots[kAppendMax];
+};
+
+__device__ __forceinline__ uint32_t e4m3x4(float a, float b, float c, float d) {
+    uint16_t lo, hi;   // cvt packs its first source operand into the upper byte
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(lo) : "f"(b), "f"(a));
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(hi) : "f"(d), "f"(c));
+    return uint32_t(lo) | (uint32_t(hi) << 16);
+}
+
+__global__ void append_f8_kernel(const __grid_constant__ AppendF8Params p) {
+    const int i = blockIdx.x, layer = blockIdx.y;
+    const int slot = p.slots[i];
+    const int page = slot >> 4, s = slot & 15;
+    const int vcol = kF8VCol(s);
+    for (int tid = threadIdx.x; tid < p.Hkv * 16; tid += blockDim.x) {
+        const int h = tid >> 4, c8 = tid & 15;
+        const long long src = ((long long)(layer)*p.T_total + p.t0 + i) * p.Hkv * 16 + (long long)h * 16 + c8;
+        const float ks = p.scale[(layer * p.Hkv + h) * 2], vs = p.scale[(layer * p.Hkv + h) * 2 + 1];
+        const uint4 kr = p.k_src[src], vr = p.v_src[src];
+        float kf[8], vf[8];
+        const uint32_t kw[4] = {kr.x, kr.y, kr.z, kr.w}, vw[4] = {vr.x, vr.y, vr.z, vr.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            kf[2 * e] = __fdiv_rn(__uint_as_float(kw[e] << 16), ks);
+            kf[2 * e + 1] = __fdiv_rn(__uint_as_float(kw[e] & 0xffff0000u), ks);
+            vf[2 * e] = __fdiv_rn(__uint_as_float(vw[e] << 16), vs);
+            vf[2 * e + 1] = __fdiv_rn(__uint_as_float(vw[e] & 0xffff0000u), vs);
+        }
+        const long long pb = layer * p.layer_stride + ((long long)page * p.Hkv + h) * 2048;
+        uint2 kc;
+        kc.x = e4m3x4(kf[0], kf[1], kf[2], kf[3]);
+        kc.y = e4m3x4(kf[4], kf[5], kf[6], kf[7]);
+        *reinterpret_cast<uint2*>(p.k_dst + pb + s * 128 + c8 * 8) = kc;
+        const uint32_t v0 = e4m3x4(vf[0], vf[1], vf[2], vf[3]), v1 = e4m3x4(vf[4], vf[5], vf[6], vf[7]);
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+            p.v_dst[pb + (c8 * 8 + e) * 16 + vcol] = uint8_t(((e < 4 ? v0 : v1) >> (8 * (e & 3))) & 0xff);
+    }
+}
+
 int launch_append(const spa_pool* pool, const void* k_new, const void* v_new, int32_t T_total,
                   const std::vector<int32_t>& slots, void* stream) {
     const auto& c = pool->cfg;
+    if (pool->kv_fp8) {
+        AppendF8Params p{};
+        p.k_src = static_cast<const uint4*>(k_new);
+        p.v_src = static_cast<const uint4*>(v_new);
+        p.k_dst = static_cast<uint8_t*>(pool->k_pool);
+        p.v_dst = static_cast<uint8_t*>(pool->v_pool);
+        p.scale = pool->kv_scale;
+        p.layer_stride = (long long)c.num_pages * c.num_kv_heads * 2048;
+        p.T_total = T_total;
+        p.Hkv = c.num_kv_heads;
+        const int threads = std::min(256, ((p.Hkv * 16 + 31) / 32) * 32);
+        for (int t0 = 0; t0 < T_total; t0 += kAppendMax) {
+            p.t0 = t0;
+            p.n = std::min(kAppendMax, T_total - t0);
+            std::memcpy(p.slots, slots.data() + t0, sizeof(int) * p.n);
+            append_f8_kernel<<<dim3(p.n, c.num_layers), threads, 0, static_cast<cudaStream_t>(stream)>>>(p);
+        }
+        return int(cudaGetLastError());
+    }
     AppendParams p{};
     p.k_src = static_cast<const uint4*>(k_new);
     p.v_src = static_cast<const uint4*>(v_new);
@@ -159,7 +254,11 @@ __global__ void cow_kernel(const uint4* __restrict__ k, const uint4* __restrict_
 
 int launch_cow(const spa_pool* pool, int32_t src_page, int32_t dst_page, int32_t rows, void* stream) {
     const auto& c = pool->cfg;
-    const int dvec = c.head_dim / 8;
+    int dvec = c.head_dim / 8;
+    if (pool->kv_fp8) {   // K rows of 128 B and the permuted V^T block: copy the whole 2-KB page blocks
+        dvec = c.head_dim / 16;
+        rows = c.page_size;
+    }
     const long long ls = (long long)c.num_pages * c.num_kv_heads * c.page_size * dvec;
     cow_kernel<<<dim3(c.num_layers, c.num_kv_heads), 128, 0, static_cast<cudaStream_t>(stream)>>>(
         static_cast<const uint4*>(pool->k_pool), static_cast<const uint4*>(pool->v_pool),

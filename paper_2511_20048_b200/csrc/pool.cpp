@@ -43,7 +43,8 @@ int32_t spa_abi_version(void) { return SPA_ABI_VERSION; }
 
 const char* spa_last_error(void) { return g_last_error.c_str(); }
 
-spa_status spa_pool_create(const spa_pool_config* cfg, void* k_pool, void* v_pool, spa_pool** out) {
+static spa_status pool_create(const spa_pool_config* cfg, void* k_pool, void* v_pool, bool fp8, const float* kv_scale,
+                              spa_pool** out) {
     if (!cfg || !out) return fail(SPA_ERR_INVALID_ARG, "null argument");
     *out = nullptr;
     const spa_pool_config& c = *cfg;
@@ -61,12 +62,20 @@ spa_status spa_pool_create(const spa_pool_config* cfg, void* k_pool, void* v_poo
             return fail(SPA_ERR_INVALID_ARG, "k_pool / v_pool must be 128-byte aligned");
         const int64_t rows = int64_t(c.num_layers) * c.num_pages * c.num_kv_heads * c.page_size;
         if (rows >= (int64_t(1) << 31)) return fail(SPA_ERR_UNSUPPORTED, "pool exceeds 2^31 rows");
+        if (fp8) {
+            if (c.head_dim != 128) return fail(SPA_ERR_UNSUPPORTED, "fp8 KV pages need head_dim 128");
+            if (!kv_scale) return fail(SPA_ERR_INVALID_ARG, "fp8 KV pages need kv_scale");
+            if (rows * (c.head_dim / c.page_size) >= (int64_t(1) << 31))
+                return fail(SPA_ERR_UNSUPPORTED, "fp8 pool exceeds 2^31 transposed V rows");
+        }
     }
     spa_pool* p = new spa_pool();
     p->cfg = c;
     p->k_pool = k_pool;
     p->v_pool = v_pool;
     p->metadata_only = !device;
+    p->kv_fp8 = fp8;
+    p->kv_scale = kv_scale;
     p->refcount.assign(c.num_pages, 0);
     for (int32_t i = 0; i < c.num_pages; ++i) p->free_set.insert(p->free_set.end(), i);
     if (device) {
@@ -91,6 +100,15 @@ spa_status spa_pool_create(const spa_pool_config* cfg, void* k_pool, void* v_poo
     }
     *out = p;
     return SPA_OK;
+}
+
+spa_status spa_pool_create(const spa_pool_config* cfg, void* k_pool, void* v_pool, spa_pool** out) {
+    return pool_create(cfg, k_pool, v_pool, false, nullptr, out);
+}
+
+spa_status spa_pool_create_fp8(const spa_pool_config* cfg, void* k_pool, void* v_pool, const float* kv_scale,
+                               spa_pool** out) {
+    return pool_create(cfg, k_pool, v_pool, true, kv_scale, out);
 }
 
 spa_status spa_pool_destroy(spa_pool* pool) {

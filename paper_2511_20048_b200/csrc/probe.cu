@@ -252,6 +252,7 @@ spa_status spa_debug_read_bw_ldg(const void* buf, size_t bytes, void* sink4, voi
 
 spa_status spa_debug_pool_read_tma(const spa_pool* pool, int32_t layers, int32_t mode, void* stream) {
     if (!pool || pool->metadata_only) return fail(SPA_ERR_INVALID_ARG, "device pool needed");
+    if (pool->kv_fp8) return fail(SPA_ERR_UNSUPPORTED, "the TMA read probe is written for bf16 pools");
     const auto& c = pool->cfg;
     if (layers <= 0 || layers > c.num_layers) return fail(SPA_ERR_INVALID_ARG, "layers out of range");
     if (mode < 0 || mode > 2) return fail(SPA_ERR_INVALID_ARG, "mode must be 0, 1 or 2");

@@ -97,6 +97,10 @@ struct spa_pool {
     std::set<int32_t> free_set;
     spa_tmap tmap_k, tmap_v;
     spa_tmap tmap_k1;   // K pool, one 64-column chunk per box (the extend kernel's key-contiguous stages)
+    // F4 (spa_pool_create_fp8): e4m3 pages, K token-major, V transposed per page with the
+    // slot permutation kF8VCol; static (k_scale, v_scale) per (layer, KV head), device fp32
+    bool kv_fp8 = false;
+    const float* kv_scale = nullptr;
 };
 
 struct spa_plan {
@@ -151,6 +155,15 @@ namespace spa {
 int launch_append(const spa_pool* pool, const void* k_new, const void* v_new, int32_t T_total,
                   const std::vector<int32_t>& dst_slots, void* stream);
 int launch_cow(const spa_pool* pool, int32_t src_page, int32_t dst_page, int32_t rows, void* stream);
+// F4: the V^T column of page slot s (0..15).  Slots (2t, 2t+1, 2t+8, 2t+9) sit in columns
+// 4t..4t+3, so one 4-B shared-memory load gives a thread its mma.m16n8k16 B fragment of PV.
+#ifdef __CUDACC__
+#define SPA_HD __host__ __device__
+#else
+#define SPA_HD
+#endif
+SPA_HD inline int kF8VCol(int s) { return 4 * ((s & 7) >> 1) + (s & 1) + 2 * (s >> 3); }
+
 struct PeerLaunch {   // F1: what the decode kernel needs to fan its outputs out and meet its peers
     int rank, world;
     long long delta[8];   // byte distance from this rank's output buffer to rank k's (mapped here)

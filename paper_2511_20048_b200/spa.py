@@ -53,6 +53,8 @@ class spa_plan_stats(ctypes.Structure):
 _SIGS = {
     "spa_pool_create": (c_int32, [ctypes.POINTER(spa_pool_config), c_void_p, c_void_p, ctypes.POINTER(c_void_p)]),
     "spa_pool_destroy": (c_int32, [c_void_p]),
+    "spa_pool_create_fp8": (c_int32, [ctypes.POINTER(spa_pool_config), c_void_p, c_void_p, c_void_p,
+                                      ctypes.POINTER(c_void_p)]),
     "spa_kv_alloc": (c_int32, [c_void_p, P_int64]),
     "spa_kv_append": (c_int32, [c_void_p, c_int32, P_int64, P_int32, c_void_p, c_void_p, c_void_p]),
     "spa_fork_request": (c_int32, [c_void_p, c_int64, c_int32, P_int64, c_void_p]),
@@ -115,6 +117,8 @@ def read_ceilings(pool: "Pool", scratch_bytes: int = 4 << 30, reps: int = 5, str
         best = max(best, buf.numel() * 2 / (ev[0].elapsed_time(ev[1]) * 1e-3) / 1e9)
     out["ldg_read_gbs"] = best
     del buf
+    if getattr(pool, "fp8", False):   # the TMA probe is bf16-only
+        return out
     c = pool.cfg
     per_layer = (c.num_pages // 2 * 2) * c.num_kv_heads * c.page_size * c.head_dim * 2 * 2
     layers = max(1, min(c.num_layers, (8 << 30) // max(1, per_layer)))
@@ -241,16 +245,34 @@ def spa_kv_page_table(pool_h, req: int):
 class Pool:
     """A paged KV pool.  device=None -> metadata-only pool (host logic only)."""
 
-    def __init__(self, num_layers, num_q_heads, num_kv_heads, head_dim, num_pages, page_size=16, device=None):
+    def __init__(self, num_layers, num_q_heads, num_kv_heads, head_dim, num_pages, page_size=16, device=None,
+                 kv_scale=None):
+        """kv_scale: fp32 [L, Hkv, 2] (k_scale, v_scale) -> an FP8 (e4m3) pool (spa_pool_create_fp8)."""
         self.cfg = spa_pool_config(num_layers, num_q_heads, num_kv_heads, head_dim, page_size, num_pages)
         self.k = self.v = None
+        self.fp8 = kv_scale is not None
+        self.kv_scale = None
         if device is not None:
             import torch  # noqa: WPS433
 
-            shape = (num_layers, num_pages, num_kv_heads, page_size, head_dim)
-            self.k = torch.empty(shape, dtype=torch.bfloat16, device=device)
-            self.v = torch.empty(shape, dtype=torch.bfloat16, device=device)
-        self.h = spa_pool_create(self.cfg, _ptr(self.k), _ptr(self.v))
+            if self.fp8:
+                self.kv_scale = torch.as_tensor(kv_scale, dtype=torch.float32).reshape(
+                    num_layers, num_kv_heads, 2).to(device).contiguous()
+                self.k = torch.empty((num_layers, num_pages, num_kv_heads, page_size, head_dim), dtype=torch.uint8,
+                                     device=device)
+                self.v = torch.empty((num_layers, num_pages, num_kv_heads, head_dim, page_size), dtype=torch.uint8,
+                                     device=device)
+            else:
+                shape = (num_layers, num_pages, num_kv_heads, page_size, head_dim)
+                self.k = torch.empty(shape, dtype=torch.bfloat16, device=device)
+                self.v = torch.empty(shape, dtype=torch.bfloat16, device=device)
+        if self.fp8:
+            h = c_void_p()
+            _check(lib().spa_pool_create_fp8(ctypes.byref(self.cfg), _ptr(self.k), _ptr(self.v), _ptr(self.kv_scale),
+                                             ctypes.byref(h)))
+            self.h = h
+        else:
+            self.h = spa_pool_create(self.cfg, _ptr(self.k), _ptr(self.v))
 
     @property
     def num_pages(self):

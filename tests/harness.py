@@ -36,7 +36,7 @@ class GpuBatch:
     """A recipe's batch built in a GPU pool through the C ABI."""
 
     def __init__(self, inputs: families.BatchInputs, num_pages=None, device="cuda", shard=(0, 1),
-                 pre_shuffle=0):
+                 pre_shuffle=0, kv_scale=None):
         m = inputs.recipe.model
         self.inputs = inputs
         self.model = m
@@ -47,7 +47,7 @@ class GpuBatch:
         self.q_sl = slice(r * self.hq_l, (r + 1) * self.hq_l)
         L = len(inputs.layers)
         self.pool = spa.Pool(L, self.hq_l, self.hkv_l, m.head_dim, num_pages or pages_needed(inputs.recipe) + pre_shuffle,
-                             device=device)
+                             device=device, kv_scale=None if kv_scale is None else kv_scale[:, self.kv_sl])
         if pre_shuffle:   # permute physical page ids: occupy, then free every other page
             junk = [self.pool.alloc() for _ in range(pre_shuffle)]
             for j in junk:
@@ -83,14 +83,28 @@ def compare(o: torch.Tensor, lse: torch.Tensor, O_ref: np.ndarray, L_ref: np.nda
     return float(np.abs(og - O_ref).max()), float(np.abs(lg - L_ref).max())
 
 
+def fp8_scales(inputs: families.BatchInputs) -> np.ndarray:
+    """Static per-(stored layer, KV head) e4m3 scales (k_scale, v_scale) = amax / 448 over
+    the batch's appended K / V (a calibration pass over the synthetic inputs)."""
+    m = inputs.recipe.model
+    amax = np.zeros((len(inputs.layers), m.num_kv_heads, 2), np.float32)
+    for oi, op in enumerate(inputs.ops):
+        if op[0] == "append":
+            for t, arr in ((0, inputs.append_k[oi]), (1, inputs.append_v[oi])):
+                x = np.abs((arr.astype(np.uint32) << 16).view(np.float32))    # [L, n, Hkv, d]
+                amax[:, :, t] = np.maximum(amax[:, :, t], x.max(axis=(1, 3)))
+    return (np.maximum(amax, 1e-3) / np.float32(448.0)).astype(np.float32)
+
+
 def run_parity(recipe, family="flat", window=0, sharing=True, max_rows=16, split_pages=0, num_ctas=0,
-               layers=None, pre_shuffle=0, merge_mode=0):
+               layers=None, pre_shuffle=0, merge_mode=0, fp8=False):
     inp = families.make_inputs(recipe, family, layers=layers)
-    gb = GpuBatch(inp, pre_shuffle=pre_shuffle)
+    scales = fp8_scales(inp) if fp8 else None
+    gb = GpuBatch(inp, pre_shuffle=pre_shuffle, kv_scale=scales)
     plan = spa.Plan(gb.pool, sharing=sharing, max_rows=max_rows, split_pages=split_pages, num_ctas=num_ctas,
                     merge_mode=merge_mode)
     plan.plan(gb.reqs, window)
-    rp = Replay(inp)
+    rp = Replay(inp, kv_fp8_scale=scales)
     errs = []
     outs = []
     for li in range(len(inp.layers)):
