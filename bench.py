@@ -64,6 +64,8 @@ def parse(argv=None):
                     help="cudaProfilerStart/Stop around the timed steps only (ncu --profile-from-start off); "
                          "skips parity, e2e and the cpu baseline")
     ap.add_argument("--sharing", type=int, default=1)
+    ap.add_argument("--kv", default="bf16", choices=["bf16", "fp8"],
+                    help="KV page format: bf16, or e4m3 with static per-(layer, head) scales (S8(f) F4 variant)")
     ap.add_argument("--gather", default="fused", choices=["fused", "nccl"],
                     help="N > 1: fused decode + peer-memory all-gather (S8(f) F1) or decode + ncclAllGather")
     ap.add_argument("--merge-mode", type=int, default=0,
@@ -116,9 +118,15 @@ def logical_kv_np(recipe, gi, who, layers, kind):
     return np.concatenate([a, b], axis=1)
 
 
-def oracle_sample(recipe, batch, rows, layer, q_bits, steps_appended, window=0):
+# F4: the counter-hash generator's values lie in [-126/32, 126/32] (spa_inputs._h2v_np), so a
+# static scale of (126/32)/448 maps every K/V value into e4m3's range without saturation
+FP8_SCALE = np.float32((126.0 / 32.0) / 448.0)
+
+
+def oracle_sample(recipe, batch, rows, layer, q_bits, steps_appended, window=0, fp8=False):
     """fp64 oracle outputs for batch rows `rows` at one (resident) layer."""
     from oracle.attention import decode_attention
+    from oracle.fp8 import dequantize_e4m3, quantize_kv
     from oracle.replay import bits_to_f64
 
     m = recipe.model
@@ -132,7 +140,11 @@ def oracle_sample(recipe, batch, rows, layer, q_bits, steps_appended, window=0):
             vb = kv_bits_np(recipe.seed, KIND_V, 500_000 + s, [layer], np.arange(len(batch)), m.num_kv_heads, m.head_dim)
             K = np.concatenate([K, kb[0, r:r + 1]])
             V = np.concatenate([V, vb[0, r:r + 1]])
-        O, L = decode_attention(bits_to_f64(q_bits[r]), bits_to_f64(K), bits_to_f64(V), m.softmax_scale, window)
+        Kf, Vf = bits_to_f64(K), bits_to_f64(V)
+        if fp8:   # the pool holds scale * e4m3(fp32(x) / scale) (oracle/fp8.py)
+            Kf = dequantize_e4m3(quantize_kv(Kf.astype(np.float32), FP8_SCALE), FP8_SCALE)
+            Vf = dequantize_e4m3(quantize_kv(Vf.astype(np.float32), FP8_SCALE), FP8_SCALE)
+        O, L = decode_attention(bits_to_f64(q_bits[r]), Kf, Vf, m.softmax_scale, window)
         out_o.append(O)
         out_l.append(L)
     return np.stack(out_o), np.stack(out_l)
@@ -278,10 +290,11 @@ def pages_for(recipe, extra_tokens):
     return pages
 
 
-def alg_bytes(st, N, hkv_l, hq_l, d):
+def alg_bytes(st, N, hkv_l, hq_l, d, kv_elem=2):
     """Algorithmic bytes of one decode_attention launch (per GPU): unique KV tokens per KV
-    head x Hkv_l x d x 2 (K, V) x 2 B + Q + O (bf16) + LSE (fp32) + partials (fp32, w+r)."""
-    kv = st["unique_tokens"] * hkv_l * d * 2 * 2
+    head x Hkv_l x d x 2 (K, V) x kv_elem B (2 bf16, 1 fp8) + Q + O (bf16) + LSE (fp32) +
+    partials (fp32, w+r)."""
+    kv = st["unique_tokens"] * hkv_l * d * 2 * kv_elem
     qo = N * hq_l * d * 2 * 2 + N * hq_l * 4
     part = st["n_records"] * hq_l * (d + 1) * 4 * 2
     return kv + qo + part
@@ -328,7 +341,9 @@ def run_spa(args):
     # non-legacy stream); torch ops use it as their current stream
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
-    pool = spa.Pool(Lr, hq_l, hkv_l, d, pages_for(recipe, total_steps), device=dev)
+    fp8 = args.kv == "fp8"
+    pool = spa.Pool(Lr, hq_l, hkv_l, d, pages_for(recipe, total_steps), device=dev,
+                    kv_scale=np.full((Lr, hkv_l, 2), FP8_SCALE, np.float32) if fp8 else None)
 
     t_build = time.perf_counter()
     ids, reqs, batch = build_batch(spa, pool, recipe, layers, kv_sl, dev)
@@ -422,7 +437,7 @@ def run_spa(args):
         for ci in calls:
             r, w = sched[ci]
             qb = kv_bits_np(recipe.seed, KIND_Q, 1_000_000, [r], np.arange(N), m.num_q_heads, d)[0]
-            O, Lo = oracle_sample(recipe, batch, rows, r, qb, steps_appended=1, window=w)
+            O, Lo = oracle_sample(recipe, batch, rows, r, qb, steps_appended=1, window=w, fp8=fp8)
             if world == 1:
                 og = o_all[ci, rows].float().cpu().numpy()
                 lg = lse_all[ci, rows].cpu().numpy()
@@ -513,7 +528,7 @@ def run_spa(args):
         st = plans[w].stats()
         per_window[w] = {"calls": len(cis), "layer_ms": float(np.median(chained)),
                          "layer_ms_isolated": float(np.median(iso)), "stats": st,
-                         "alg_bytes": alg_bytes(st, N, hkv_l, hq_l, d)}
+                         "alg_bytes": alg_bytes(st, N, hkv_l, hq_l, d, 1 if fp8 else 2)}
     _log('per-window timing done')
     # the dominant launch class: most total time per step
     wdom = max(windows, key=lambda w: per_window[w]["layer_ms"] * per_window[w]["calls"])
@@ -526,7 +541,7 @@ def run_spa(args):
     traffic = None
     try:
         nc = json.load(open(os.path.join(ROOT, "profiles", "latest_ncu.json")))
-        if nc.get("config") == args.config and world == 1 and args.sharing:
+        if nc.get("config") == args.config and world == 1 and args.sharing and not fp8:
             traffic = nc["traffic_bytes_per_launch"]
     except (OSError, ValueError, KeyError):
         pass
@@ -626,7 +641,7 @@ def run_spa(args):
             "higher_is_better": True,
             "scaling": "strong",
             "vs_baseline": None,
-            "dtype": "bf16",
+            "dtype": "bf16 (KV pages e4m3, f16 MMA)" if fp8 else "bf16",
             "data": "synthetic (seeded counter-hash bf16 K/V/Q, agent-shaped batch recipe)",
             "config": {"workload": f"{recipe.name} (BJ config {BJ_INDEX[args.config]})",
                        "n_requests": N, "agents": len(recipe.groups), "layer_calls_per_step": C,
@@ -634,6 +649,7 @@ def run_spa(args):
                        "q_heads": m.num_q_heads, "kv_heads": m.num_kv_heads, "head_dim": d,
                        "parallelism": f"kv-head sharded x{world}" if world > 1 else "1 GPU",
                        "gather": gather,
+                       "kv_pages": f"e4m3, static scale {float(FP8_SCALE):.6g} per (layer, KV head)" if fp8 else "bf16",
                        "sharing": bool(args.sharing), "cuda_graph": bool(args.graph),
                        "l2": "inputs larger than L2 (the KV a step's calls read > 4 x 126 MB, layers rotate), no flush"
                        if ws_step > 4 * 126e6 else "KV of a step fits L2: latency, not bandwidth"},
@@ -651,7 +667,8 @@ def run_spa(args):
                          "peak_kind": pk_kind, "alg_bytes_per_launch": int(dom["alg_bytes"]),
                          "frac_of_8tbs": achieved / 8000.0,
                          "same_run_read_ceilings_gbs": ceilings,
-                         "frac_of_tma_ceiling": (achieved / ceilings["tma_pool_read_gbs"]) if ceilings else None},
+                         "frac_of_tma_ceiling": (achieved / ceilings["tma_pool_read_gbs"])
+                         if ceilings and "tma_pool_read_gbs" in ceilings else None},
             "sharing": {"unique_tokens_per_kv_head": st["unique_tokens"],
                         "unshared_tokens_per_kv_head": st["unshared_tokens"],
                         "bytes_vs_unshared": st["unique_tokens"] / st["unshared_tokens"]},

@@ -93,7 +93,7 @@ spa_status spa_pool_destroy(spa_pool* pool);
  *   v_pool: e4m3 [L][num_pages][Hkv][128][16]: each (page, head) block TRANSPOSED, and
  *     page slot s stored in column 4((s mod 8) div 2) + (s mod 2) + 2(s div 8), so the
  *     decode kernel's f16 MMA fragments are single 4-byte loads.
- *   Both 128-byte aligned, num_layers * num_pages * Hkv * 16 * 8 < 2^31.
+ *   Both 128-byte aligned, num_layers * num_pages * Hkv * 16 < 2^31.
  * Decode plans over it must use max_rows <= 64 (the tcgen05 extend kernel is bf16 only:
  * CUDA error "operation not supported" at launch otherwise). */
 spa_status spa_pool_create_fp8(const spa_pool_config* cfg, void* k_pool, void* v_pool, const float* kv_scale,

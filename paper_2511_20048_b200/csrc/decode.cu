@@ -248,9 +248,7 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8>::WARPS * 32, 
             for (int j = 0; j < PPS; ++j) {
                 if (j < npg) {
                     tma_load_3d(sb + j * 2 * C::PAGE_BYTES, &tmk, 0, row[j], 0, fb, policy);
-                    // fp8: V^T rows are d channels of a page-head, D of them per page-head
-                    tma_load_3d(sb + j * 2 * C::PAGE_BYTES + C::PAGE_BYTES, &tmv, 0, F8 ? row[j] * (D / 16) : row[j],
-                                0, fb, policy);
+                    tma_load_3d(sb + j * 2 * C::PAGE_BYTES + C::PAGE_BYTES, &tmv, 0, row[j], 0, fb, policy);
                 }
             }
         }
@@ -349,8 +347,8 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8>::WARPS * 32, 
         hi_warp = min(hi_warp, dsc.tok_end);
         float scale_l2 = p.scale_log2, v_scale = 1.f;
         if (F8) {   // K = k_scale * code folds into the logit scale, V = v_scale * code into 1/l
-            scale_l2 *= __ldg(p.kv_scale + (p.layer * Hkv + itm.kv_head) * 2);
-            v_scale = __ldg(p.kv_scale + (p.layer * Hkv + itm.kv_head) * 2 + 1);
+            scale_l2 *= __ldg(p.kv_scale + (p.layer * Hkv + itm.kv_head) * 2) * kF8Unit;
+            v_scale = __ldg(p.kv_scale + (p.layer * Hkv + itm.kv_head) * 2 + 1) * kF8Unit;
         }
         // running max per row, log2 units, raised lazily (only when a page's max exceeds it
         // by > kRescale, so P <= 2^kRescale); the same m is used for P, l and the LSE.
@@ -759,16 +757,21 @@ static int launch_decode_t(const spa_plan* P, const DecodeParams& dp, void* stre
                       *tk, *tv, dp);
 }
 
-// F4 fp8 pages (d = 128): the same team shapes as bf16
+// F4 fp8 pages (d = 128): the same team shapes as bf16; SPA_F8_PPS pages per stage (4: the
+// same 16-KB stages as bf16, two pages per warp per stage for ILP; 2 measured 12 % slower)
+#ifndef SPA_F8_PPS
+#define SPA_F8_PPS 4
+#endif
 static int launch_decode_f8(const spa_plan* P, const DecodeParams& dp, void* stream) {
+    constexpr int S = SPA_F8_PPS;
     if (P->mt == 1) {
-        if (P->teams == 1) return launch_decode_t<128, 1, 2, 1, true>(P, dp, stream);
-        if (P->teams == 2) return launch_decode_t<128, 1, 2, 2, true>(P, dp, stream);
-        return launch_decode_t<128, 1, 2, 4, true>(P, dp, stream);
+        if (P->teams == 1) return launch_decode_t<128, 1, S, 1, true>(P, dp, stream);
+        if (P->teams == 2) return launch_decode_t<128, 1, S, 2, true>(P, dp, stream);
+        return launch_decode_t<128, 1, S, 4, true>(P, dp, stream);
     }
-    if (P->mt == 4) return launch_decode_t<128, 4, 2, 1, true>(P, dp, stream);
-    if (P->teams == 1) return launch_decode_t<128, 2, 2, 1, true>(P, dp, stream);
-    return launch_decode_t<128, 2, 2, 2, true>(P, dp, stream);
+    if (P->mt == 4) return launch_decode_t<128, 4, S, 1, true>(P, dp, stream);
+    if (P->teams == 1) return launch_decode_t<128, 2, S, 1, true>(P, dp, stream);
+    return launch_decode_t<128, 2, S, 2, true>(P, dp, stream);
 }
 
 template <int D>

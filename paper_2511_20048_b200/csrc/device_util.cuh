@@ -88,9 +88,24 @@ __device__ __forceinline__ void mma16816_f16(float* c, const uint32_t* a, uint32
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+#ifndef SPA_F8_INTCVT
+#define SPA_F8_INTCVT 0
+#endif
+// Two e4m3 codes (bits 7:0 -> low half, 15:8 -> high half) as f16x2.  SPA_F8_INTCVT = 0: the
+// hardware conversion (value exact).  SPA_F8_INTCVT = 1: integer bit moves -- each code's
+// byte at the top of its half, shifted right once, the sign carried back up -- which yield
+// value * 2^-8 exactly (normals and subnormals; kF8Unit) for the caller to fold into its scales.
+constexpr float kF8Unit = SPA_F8_INTCVT ? 256.f : 1.f;
 __device__ __forceinline__ uint32_t e4m3x2_to_f16x2(uint32_t two_codes) {   // low byte -> low half
     uint32_t r;
+#if SPA_F8_INTCVT
+    uint32_t x;
+    asm("prmt.b32 %0, %1, 0, 0x1404;" : "=r"(x) : "r"(two_codes));   // halves (b0 << 8, b1 << 8)
+    const uint32_t y = x >> 1;                                       // sign lands on bit 14
+    r = y + (y & 0x40004000u);                                       // ... and carries into bit 15
+#else
     asm("{ .reg .b16 t; cvt.u16.u32 t, %1; cvt.rn.f16x2.e4m3x2 %0, t; }" : "=r"(r) : "r"(two_codes));
+#endif
     return r;
 }
 

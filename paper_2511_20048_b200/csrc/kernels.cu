@@ -77,21 +77,22 @@ bool make_tensor_maps(spa_pool* p, std::string* err) {
     const auto& c = p->cfg;
     const cuuint64_t rows = cuuint64_t(c.num_layers) * c.num_pages * c.num_kv_heads * c.page_size;
     if (p->kv_fp8) {
-        // F4, d = 128: K rows of 128 e4m3 bytes, one (page, head) = a 128 x 16 box with
-        // 128-B swizzle; V^T rows of 16 bytes (one d channel of a page's 16 slots), one
-        // (page, head) = a 16 x 128 box, unswizzled (the kernel's 4-B loads of 8 rows x 16 B
-        // are conflict-free as laid out).  A unit third dimension keeps the 3-D TMA call.
-        const cuuint64_t vrows = rows * cuuint64_t(c.head_dim / c.page_size);
-        cuuint64_t kd[3] = {128, rows, 1}, vd[3] = {16, vrows, 1};
-        cuuint64_t ks[2] = {128, rows * 128}, vs[2] = {16, vrows * 16};
-        cuuint32_t kb[3] = {128, 16, 1}, vb[3] = {16, 128, 1};
+        // F4, d = 128: both pools as rows of 128 bytes -- K: one token of one head; V: 8
+        // channels x 16 slots of a page-head's transposed block -- so one (page, head) is a
+        // 128 x 16 box in both (2 KB, one TMA op; a 16-B-wide box would cost 128 row
+        // requests).  K lands 128-B swizzled (conflict-free 4-B fragment loads); V^T lands
+        // as is (8 channel rows x 16 B per 128-B line: the fragment loads are conflict-free).
+        // A unit third dimension keeps the 3-D TMA call of the bf16 maps.
+        cuuint64_t kd[3] = {128, rows, 1};
+        cuuint64_t ks[2] = {128, rows * 128};
+        cuuint32_t kb[3] = {128, 16, 1};
         cuuint32_t estr[3] = {1, 1, 1};
         CUresult r = enc(reinterpret_cast<CUtensorMap*>(p->tmap_k.bytes), CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, p->k_pool,
                          kd, ks, kb, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r == CUDA_SUCCESS)
-            r = enc(reinterpret_cast<CUtensorMap*>(p->tmap_v.bytes), CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, p->v_pool, vd,
-                    vs, vb, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            r = enc(reinterpret_cast<CUtensorMap*>(p->tmap_v.bytes), CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, p->v_pool, kd,
+                    ks, kb, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) {
             *err = "CUresult " + std::to_string(int(r));

@@ -65,8 +65,6 @@ static spa_status pool_create(const spa_pool_config* cfg, void* k_pool, void* v_
         if (fp8) {
             if (c.head_dim != 128) return fail(SPA_ERR_UNSUPPORTED, "fp8 KV pages need head_dim 128");
             if (!kv_scale) return fail(SPA_ERR_INVALID_ARG, "fp8 KV pages need kv_scale");
-            if (rows * (c.head_dim / c.page_size) >= (int64_t(1) << 31))
-                return fail(SPA_ERR_UNSUPPORTED, "fp8 pool exceeds 2^31 transposed V rows");
         }
     }
     spa_pool* p = new spa_pool();
