@@ -14,6 +14,10 @@ Contents
   kvmodel.py    a dense logical KV model (a fork is a physical copy) plus an independent
                 model of the documented paging policy (lowest-free page id, refcounts,
                 copy-on-write of the partial last page).
+  fp8.py        the e4m3 KV quantiser and dequantiser of the FP8-page variant (S8(f) F4),
+                from the format definition (round to nearest even, saturating).
+  replay.py     replays a batch's allocator call log on the models above and evaluates
+                the expected outputs (optionally on FP8-quantised K/V).
 
 Where the paper is silent (it never mentions attention, KV caches or pages -- see
 SURVEY.md Sec. 0.1) the readings used here are listed in DESIGN.md Sec. 3 and cited
