@@ -363,14 +363,36 @@ def run_spa(args):
     if world > 1 and args.gather == "fused":
         # F1: the library's peer region holds 3C gathered buffers (the e2e leg rotates three
         # output sets); handles are all-gathered over the process group
+        # every stage is agreed collectively, so a failure on one rank sends ALL ranks to NCCL
+        def agree(flag):
+            t = torch.tensor([1 if flag else 0], device="cpu" if share else dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            return bool(t.item())
+
+        why = ""
+        handle = None
         try:
-            peer = spa.Peer(rank, world, spa.Peer.buffer_bytes(N, m.num_q_heads, d), n_bufs=3 * C)
-            o_views, l_views = peer.views_all(N, m.num_q_heads, d, device=dev)
+            peer = spa.Peer(rank, world, spa.Peer.buffer_bytes(N, m.num_q_heads, d), n_bufs=3 * C, connect=False)
+            handle = peer.ipc_handle()
+        except Exception as e:  # noqa: BLE001 -- fall back to NCCL, reported in the JSON line
+            why = repr(e)
+        if agree(handle is not None):
+            handles = [None] * world
+            dist.all_gather_object(handles, handle)
+            try:
+                peer.connect(handles)
+                o_views, l_views = peer.views_all(N, m.num_q_heads, d, device=dev)
+            except Exception as e:  # noqa: BLE001
+                why = repr(e)
+        if not agree(not why):
+            if peer is not None:
+                dist.barrier()
+                peer.close()
+            peer = None
+            gather = f"nccl (fused setup failed: {why[:120] or 'on another rank'})"
+        else:
             o_all, lse_all = o_views[:C], l_views[:C]
             gather = "fused decode + peer-memory all-gather (CUDA IPC over NVLink)"
-        except Exception as e:  # noqa: BLE001 -- fall back to NCCL, reported in the JSON line
-            gather = f"nccl (fused setup failed: {e!r:.120})"
-            peer = None
     if world > 1 and peer is None:
         comm_id = [spa.spa_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(comm_id, src=0)
@@ -420,6 +442,28 @@ def run_spa(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    # ---- fused gather: one probe call first (a peer that never arrives costs the kernel's
+    #      20-s timeout once, not once per call); every rank must agree, else all use NCCL
+    if peer is not None:
+        pool.append(reqs, [1] * N, step_k[0], step_v[0], stream=stream)
+        for w, p in plans.items():
+            p.plan(reqs, w, stream=stream)
+        launch(0, q_all, o_all, lse_all)
+        torch.cuda.synchronize()
+        state["step"] = 1
+        ok = torch.tensor([1 if peer.status() == 0 else 0], device="cpu" if share else dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            barrier()
+            peer.close()
+            peer = None
+            gather = "nccl (the fused gather's probe call timed out)"
+            comm_id = [spa.spa_nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(comm_id, src=0)
+            comm = spa.Comm(comm_id[0], rank, world)
+            o_all = torch.empty((C, m.num_q_heads, N, d), dtype=torch.bfloat16, device=dev)
+            lse_all = torch.empty((C, m.num_q_heads, N), dtype=torch.float32, device=dev)
+
     # ---- parity gate: the first step's sampled outputs vs the fp64 oracle
     parity = None
     one_step(step_k, step_v)
@@ -437,7 +481,7 @@ def run_spa(args):
         for ci in calls:
             r, w = sched[ci]
             qb = kv_bits_np(recipe.seed, KIND_Q, 1_000_000, [r], np.arange(N), m.num_q_heads, d)[0]
-            O, Lo = oracle_sample(recipe, batch, rows, r, qb, steps_appended=1, window=w, fp8=fp8)
+            O, Lo = oracle_sample(recipe, batch, rows, r, qb, steps_appended=state["step"], window=w, fp8=fp8)
             if world == 1:
                 og = o_all[ci, rows].float().cpu().numpy()
                 lg = lse_all[ci, rows].cpu().numpy()

@@ -501,12 +501,20 @@ class Peer:
         if world > 1 and connect:
             import torch.distributed as dist  # noqa: WPS433
 
-            mine = ctypes.create_string_buffer(64)
-            _check(lib().spa_peer_ipc_handle(self.h, mine))
             allh = [None] * world
-            dist.all_gather_object(allh, mine.raw, group=group)
-            blob = ctypes.create_string_buffer(b"".join(allh), 64 * world)
-            _check(lib().spa_peer_connect(self.h, blob))
+            dist.all_gather_object(allh, self.ipc_handle(), group=group)
+            self.connect(allh)
+
+    def ipc_handle(self) -> bytes:
+        """This rank's 64-byte CUDA IPC handle of its region."""
+        mine = ctypes.create_string_buffer(64)
+        _check(lib().spa_peer_ipc_handle(self.h, mine))
+        return mine.raw
+
+    def connect(self, handles):
+        """Open every other rank's region (handles in rank order)."""
+        blob = ctypes.create_string_buffer(b"".join(handles), 64 * self.world)
+        _check(lib().spa_peer_connect(self.h, blob))
 
     @staticmethod
     def local_world(world: int, buf_bytes: int, n_bufs: int = 2) -> list["Peer"]:
