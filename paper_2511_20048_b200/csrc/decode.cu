@@ -110,7 +110,9 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8>::WARPS * 32, 
     constexpr int NT = D / 8;      // n8 tiles of the output
     constexpr int NTH = NT / 2;    // n8 tiles per column half
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-B aligned by pointer arithmetic on the shared array (not through an integer cast),
+    // so the compiler keeps the shared address space: LDS/STS instead of generic LD/ST
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
 
     const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0);   // provably warp-uniform
     const int lane = threadIdx.x & 31;
@@ -362,7 +364,11 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8>::WARPS * 32, 
         for (int st = 0; st < nst; ++st) {
             if (st > 0) mbar_wait(full_bar(slot), phase);
             const int npg = min(PPS, dsc.n_pages - st * PPS);
-            if (active) {
+#ifndef SPA_F8_EXP
+#define SPA_F8_EXP 0
+#endif
+            // SPA_F8_EXP = 1 (timing experiments only, wrong results): fp8 consumers skip the math
+            if (active && !(F8 && SPA_F8_EXP == 1)) {
                 const uint32_t sb = ring + slot * C::STAGE_BYTES;
                 float s[JW][2][4];
 #pragma unroll
