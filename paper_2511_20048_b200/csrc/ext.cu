@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
         // PV of a stage is issued LAG stages after its S (S_g is queued before P_{g-2} is
         // awaited), so each softmax warpgroup finds its next S ready when it finishes one
         constexpr int LAG = 2;
-        int lag_slot[LAG + 1], lag_npg[LAG + 1], lag_g[LAG + 1];   // pending stages (one pushed before a retire)
+        int lag_slot[LAG + 1] = {}, lag_npg[LAG + 1] = {}, lag_g[LAG + 1] = {};   // pending stages (one pushed before a retire)
         int n_lag = 0;
         auto retire = [&]() {   // wait for the oldest pending stage's P, then O_b += P V
             const int gg = lag_g[0], b = gg & 1, ps = lag_slot[0], pn = lag_npg[0];
