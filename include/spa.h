@@ -89,15 +89,15 @@ spa_status spa_pool_destroy(spa_pool* pool);
  *     in:  code = e4m3 round-to-nearest-even, saturating at +-448, of fp32(x) / scale
  *     (IEEE fp32 division; oracle/fp8.py), and decode reads K = k_scale * code,
  *     V = v_scale * code.
- *   k_pool: e4m3 [L][num_pages][Hkv][16][128] (token-major rows, as bf16 pools).
- *   v_pool: e4m3 [L][num_pages][Hkv][128][16]: each (page, head) block TRANSPOSED, and
- *     page slot s stored in column 4((s mod 8) div 2) + (s mod 2) + 2(s div 8), so the
- *     decode kernel's f16 MMA fragments are single 4-byte loads.
- *   Both 128-byte aligned, num_layers * num_pages * Hkv * 16 < 2^31.
+ *   kv_pool: ONE caller-owned buffer, e4m3 [L][num_pages][Hkv][2][2048 B], 128-byte
+ *     aligned: per (page, head) the K block [16 slots][128 ch] (token-major rows, as bf16
+ *     pools) followed by the V block TRANSPOSED, [128 ch][16 slots], page slot s stored in
+ *     column 4((s mod 8) div 2) + (s mod 2) + 2(s div 8) -- so a page-head's K and V are one
+ *     4-KB TMA box and the decode kernel's f16 MMA fragments are single 4-byte loads.
+ *     num_layers * num_pages * Hkv * 32 < 2^31.  (NULL: a metadata-only pool.)
  * Decode plans over it must use max_rows <= 64 (the tcgen05 extend kernel is bf16 only:
  * CUDA error "operation not supported" at launch otherwise). */
-spa_status spa_pool_create_fp8(const spa_pool_config* cfg, void* k_pool, void* v_pool, const float* kv_scale,
-                               spa_pool** out);
+spa_status spa_pool_create_fp8(const spa_pool_config* cfg, void* kv_pool, const float* kv_scale, spa_pool** out);
 
 /* a1: a new, empty request (length 0, no pages). */
 spa_status spa_kv_alloc(spa_pool* pool, spa_req* out_req);

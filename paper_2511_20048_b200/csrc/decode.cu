@@ -249,8 +249,12 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8>::WARPS * 32, 
 #pragma unroll
             for (int j = 0; j < PPS; ++j) {
                 if (j < npg) {
-                    tma_load_3d(sb + j * 2 * C::PAGE_BYTES, &tmk, 0, row[j], 0, fb, policy);
-                    tma_load_3d(sb + j * 2 * C::PAGE_BYTES + C::PAGE_BYTES, &tmv, 0, row[j], 0, fb, policy);
+                    if constexpr (F8) {   // one box: the page-head's K rows then its V^T rows (4 KB)
+                        tma_load_3d(sb + j * 2 * C::PAGE_BYTES, &tmk, 0, 2 * row[j], 0, fb, policy);
+                    } else {
+                        tma_load_3d(sb + j * 2 * C::PAGE_BYTES, &tmk, 0, row[j], 0, fb, policy);
+                        tma_load_3d(sb + j * 2 * C::PAGE_BYTES + C::PAGE_BYTES, &tmv, 0, row[j], 0, fb, policy);
+                    }
                 }
             }
         }
@@ -510,11 +514,13 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8>::WARPS * 32, 
                         }
                         const uint32_t vb = sb + j * 2 * C::PAGE_BYTES + C::PAGE_BYTES;
                         if constexpr (F8) {
-                            // V^T rows of 16 slot bytes (columns kF8VCol): channel n*8 + g, slots
-                            // (2t, 2t+1, 2t+8, 2t+9) at 4t..4t+3 -> the f16 B fragment of PV
+                            // V^T: channel n*8 + g is 16-B chunk g of 128-B row n (swizzled: g ^ n),
+                            // slots (2t, 2t+1, 2t+8, 2t+9) at bytes 4t..4t+3 of it (kF8VCol) -> the
+                            // f16 B fragment of PV in one 4-B load
 #pragma unroll
                             for (int n = 0; n < NT; ++n) {
-                                const uint32_t w = lds32(vb + (n * 8 + (lane >> 2)) * 16 + 4 * (lane & 3));
+                                const uint32_t w =
+                                    lds32(vb + n * 128 + ((((lane >> 2) ^ n) & 7) << 4) + 4 * (lane & 3));
                                 mma16816_f16(acc[n], pa, e4m3x2_to_f16x2(w), e4m3x2_to_f16x2(w >> 16));
                             }
                         } else {

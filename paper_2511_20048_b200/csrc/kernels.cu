@@ -38,12 +38,13 @@ const char* cuda_error_string(int err) { return cudaGetErrorString(cudaError_t(e
 
 static size_t pool_bytes(const spa_pool* p) {
     const auto& c = p->cfg;
-    return size_t(c.num_layers) * c.num_pages * c.num_kv_heads * c.page_size * c.head_dim * (p->kv_fp8 ? 1 : 2);
+    return size_t(c.num_layers) * c.num_pages * c.num_kv_heads * c.page_size * c.head_dim * 2;
 }
 
 int memset_pool(spa_pool* p) {
+    // fp8: ONE interleaved buffer of the same byte size (K and V^T blocks alternate per page-head)
     cudaError_t e = cudaMemset(p->k_pool, 0, pool_bytes(p));
-    if (e == cudaSuccess) e = cudaMemset(p->v_pool, 0, pool_bytes(p));
+    if (e == cudaSuccess && !p->kv_fp8) e = cudaMemset(p->v_pool, 0, pool_bytes(p));
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     return int(e);
 }
@@ -77,23 +78,19 @@ bool make_tensor_maps(spa_pool* p, std::string* err) {
     const auto& c = p->cfg;
     const cuuint64_t rows = cuuint64_t(c.num_layers) * c.num_pages * c.num_kv_heads * c.page_size;
     if (p->kv_fp8) {
-        // F4, d = 128: both pools as rows of 128 bytes -- K: one token of one head; V: 8
-        // channels x 16 slots of a page-head's transposed block -- so one (page, head) is a
-        // 128 x 16 box in both (2 KB, one TMA op; a 16-B-wide box would cost 128 row
-        // requests).  K lands 128-B swizzled (conflict-free 4-B fragment loads); V^T lands
-        // as is (8 channel rows x 16 B per 128-B line: the fragment loads are conflict-free).
+        // F4, d = 128: the interleaved buffer as rows of 128 bytes -- 16 K rows (one token
+        // each) then 16 V^T rows (8 channels x 16 slots each) per page-head -- so a whole
+        // page-head, K and V, is ONE 128 x 32 box (4 KB, as a bf16 page-head's K box), landing
+        // 128-B swizzled (the kernel's 4-B fragment loads are conflict-free through the XOR).
         // A unit third dimension keeps the 3-D TMA call of the bf16 maps.
-        cuuint64_t kd[3] = {128, rows, 1};
-        cuuint64_t ks[2] = {128, rows * 128};
-        cuuint32_t kb[3] = {128, 16, 1};
+        cuuint64_t kd[3] = {128, rows * 2, 1};
+        cuuint64_t ks[2] = {128, rows * 2 * 128};
+        cuuint32_t kb[3] = {128, 32, 1};
         cuuint32_t estr[3] = {1, 1, 1};
         CUresult r = enc(reinterpret_cast<CUtensorMap*>(p->tmap_k.bytes), CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, p->k_pool,
                          kd, ks, kb, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r == CUDA_SUCCESS)
-            r = enc(reinterpret_cast<CUtensorMap*>(p->tmap_v.bytes), CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, p->v_pool, kd,
-                    ks, kb, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        std::memcpy(p->tmap_v.bytes, p->tmap_k.bytes, sizeof(p->tmap_v.bytes));
         if (r != CUDA_SUCCESS) {
             *err = "CUresult " + std::to_string(int(r));
             return false;
@@ -153,10 +150,9 @@ __global__ void append_kernel(const __grid_constant__ AppendParams p) {
 struct AppendF8Params {
     const uint4* k_src;
     const uint4* v_src;
-    uint8_t* k_dst;
-    uint8_t* v_dst;
+    uint8_t* k_dst;          // the interleaved buffer
     const float* scale;      // [L][Hkv][2]
-    long long layer_stride;  // bytes: num_pages * Hkv * 16 * 128
+    long long layer_stride;  // bytes: num_pages * Hkv * 4096 (interleaved K / V^T blocks)
     int T_total, t0, n, Hkv;
     int slots[kAppendMax];
 };
@@ -187,7 +183,7 @@ __global__ void append_f8_kernel(const __grid_constant__ AppendF8Params p) {
             vf[2 * e] = __fdiv_rn(__uint_as_float(vw[e] << 16), vs);
             vf[2 * e + 1] = __fdiv_rn(__uint_as_float(vw[e] & 0xffff0000u), vs);
         }
-        const long long pb = layer * p.layer_stride + ((long long)page * p.Hkv + h) * 2048;
+        const long long pb = layer * p.layer_stride + ((long long)page * p.Hkv + h) * 4096;
         uint2 kc;
         kc.x = e4m3x4(kf[0], kf[1], kf[2], kf[3]);
         kc.y = e4m3x4(kf[4], kf[5], kf[6], kf[7]);
@@ -195,7 +191,7 @@ __global__ void append_f8_kernel(const __grid_constant__ AppendF8Params p) {
         const uint32_t v0 = e4m3x4(vf[0], vf[1], vf[2], vf[3]), v1 = e4m3x4(vf[4], vf[5], vf[6], vf[7]);
 #pragma unroll
         for (int e = 0; e < 8; ++e)
-            p.v_dst[pb + (c8 * 8 + e) * 16 + vcol] = uint8_t(((e < 4 ? v0 : v1) >> (8 * (e & 3))) & 0xff);
+            p.k_dst[pb + 2048 + (c8 * 8 + e) * 16 + vcol] = uint8_t(((e < 4 ? v0 : v1) >> (8 * (e & 3))) & 0xff);
     }
 }
 
@@ -207,9 +203,8 @@ int launch_append(const spa_pool* pool, const void* k_new, const void* v_new, in
         p.k_src = static_cast<const uint4*>(k_new);
         p.v_src = static_cast<const uint4*>(v_new);
         p.k_dst = static_cast<uint8_t*>(pool->k_pool);
-        p.v_dst = static_cast<uint8_t*>(pool->v_pool);
         p.scale = pool->kv_scale;
-        p.layer_stride = (long long)c.num_pages * c.num_kv_heads * 2048;
+        p.layer_stride = (long long)c.num_pages * c.num_kv_heads * 4096;
         p.T_total = T_total;
         p.Hkv = c.num_kv_heads;
         const int threads = std::min(256, ((p.Hkv * 16 + 31) / 32) * 32);
@@ -256,9 +251,16 @@ __global__ void cow_kernel(const uint4* __restrict__ k, const uint4* __restrict_
 int launch_cow(const spa_pool* pool, int32_t src_page, int32_t dst_page, int32_t rows, void* stream) {
     const auto& c = pool->cfg;
     int dvec = c.head_dim / 8;
-    if (pool->kv_fp8) {   // K rows of 128 B and the permuted V^T block: copy the whole 2-KB page blocks
-        dvec = c.head_dim / 16;
-        rows = c.page_size;
+    if (pool->kv_fp8) {
+        // interleaved 4-KB page-head blocks (K rows + the permuted V^T block): copy them whole
+        // as 32 "rows" of 128 B of the one buffer (slots past the fork point are overwritten
+        // by the child's appends before they are read)
+        const long long ls = (long long)c.num_pages * c.num_kv_heads * 256;   // uint4 per layer
+        cow_kernel<<<dim3(c.num_layers, c.num_kv_heads), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+            static_cast<const uint4*>(pool->k_pool), static_cast<const uint4*>(pool->k_pool),
+            static_cast<uint4*>(pool->k_pool), static_cast<uint4*>(pool->k_pool), ls, src_page, dst_page, 32,
+            c.num_kv_heads, 8, 32);
+        return int(cudaGetLastError());
     }
     const long long ls = (long long)c.num_pages * c.num_kv_heads * c.page_size * dvec;
     cow_kernel<<<dim3(c.num_layers, c.num_kv_heads), 128, 0, static_cast<cudaStream_t>(stream)>>>(

@@ -65,6 +65,7 @@ static spa_status pool_create(const spa_pool_config* cfg, void* k_pool, void* v_
         if (fp8) {
             if (c.head_dim != 128) return fail(SPA_ERR_UNSUPPORTED, "fp8 KV pages need head_dim 128");
             if (!kv_scale) return fail(SPA_ERR_INVALID_ARG, "fp8 KV pages need kv_scale");
+            if (rows * 2 >= (int64_t(1) << 31)) return fail(SPA_ERR_UNSUPPORTED, "fp8 pool exceeds 2^31 128-B rows");
         }
     }
     spa_pool* p = new spa_pool();
@@ -104,9 +105,9 @@ spa_status spa_pool_create(const spa_pool_config* cfg, void* k_pool, void* v_poo
     return pool_create(cfg, k_pool, v_pool, false, nullptr, out);
 }
 
-spa_status spa_pool_create_fp8(const spa_pool_config* cfg, void* k_pool, void* v_pool, const float* kv_scale,
-                               spa_pool** out) {
-    return pool_create(cfg, k_pool, v_pool, true, kv_scale, out);
+spa_status spa_pool_create_fp8(const spa_pool_config* cfg, void* kv_pool, const float* kv_scale, spa_pool** out) {
+    // one interleaved buffer: page-head blocks of 4 KB = K (2 KB) then V^T (2 KB)
+    return pool_create(cfg, kv_pool, kv_pool ? static_cast<char*>(kv_pool) + 2048 : nullptr, true, kv_scale, out);
 }
 
 spa_status spa_pool_destroy(spa_pool* pool) {

@@ -53,8 +53,7 @@ class spa_plan_stats(ctypes.Structure):
 _SIGS = {
     "spa_pool_create": (c_int32, [ctypes.POINTER(spa_pool_config), c_void_p, c_void_p, ctypes.POINTER(c_void_p)]),
     "spa_pool_destroy": (c_int32, [c_void_p]),
-    "spa_pool_create_fp8": (c_int32, [ctypes.POINTER(spa_pool_config), c_void_p, c_void_p, c_void_p,
-                                      ctypes.POINTER(c_void_p)]),
+    "spa_pool_create_fp8": (c_int32, [ctypes.POINTER(spa_pool_config), c_void_p, c_void_p, ctypes.POINTER(c_void_p)]),
     "spa_kv_alloc": (c_int32, [c_void_p, P_int64]),
     "spa_kv_append": (c_int32, [c_void_p, c_int32, P_int64, P_int32, c_void_p, c_void_p, c_void_p]),
     "spa_fork_request": (c_int32, [c_void_p, c_int64, c_int32, P_int64, c_void_p]),
@@ -258,18 +257,19 @@ class Pool:
             if self.fp8:
                 self.kv_scale = torch.as_tensor(kv_scale, dtype=torch.float32).reshape(
                     num_layers, num_kv_heads, 2).to(device).contiguous()
-                self.k = torch.empty((num_layers, num_pages, num_kv_heads, page_size, head_dim), dtype=torch.uint8,
-                                     device=device)
-                self.v = torch.empty((num_layers, num_pages, num_kv_heads, head_dim, page_size), dtype=torch.uint8,
-                                     device=device)
+                # one interleaved buffer: per page-head the K block then the transposed V block
+                self.kv = torch.empty((num_layers, num_pages, num_kv_heads, 2, page_size, head_dim),
+                                      dtype=torch.uint8, device=device)
+                self.k = self.kv[:, :, :, 0]                                       # [L, P, Hkv, 16, d]
+                self.v = self.kv[:, :, :, 1].view(num_layers, num_pages, num_kv_heads, head_dim, page_size)
             else:
                 shape = (num_layers, num_pages, num_kv_heads, page_size, head_dim)
                 self.k = torch.empty(shape, dtype=torch.bfloat16, device=device)
                 self.v = torch.empty(shape, dtype=torch.bfloat16, device=device)
         if self.fp8:
             h = c_void_p()
-            _check(lib().spa_pool_create_fp8(ctypes.byref(self.cfg), _ptr(self.k), _ptr(self.v), _ptr(self.kv_scale),
-                                             ctypes.byref(h)))
+            _check(lib().spa_pool_create_fp8(ctypes.byref(self.cfg), _ptr(getattr(self, "kv", None)),
+                                             _ptr(self.kv_scale), ctypes.byref(h)))
             self.h = h
         else:
             self.h = spa_pool_create(self.cfg, _ptr(self.k), _ptr(self.v))
