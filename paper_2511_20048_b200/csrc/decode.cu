@@ -400,8 +400,9 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8>::WARPS * 32, 
                                 for (int nt = 0; nt < 2; ++nt) {
                                     const int kr = nt * 8 + (lane >> 2);
                                     const uint32_t w = lds32(kb + kr * 128 + (((ks ^ kr) & 7) << 4) + 4 * (lane & 3));
-                                    mma16816_f16(sc[ks % kQkChains][nt], qa[ks], e4m3x2_to_f16x2(w),
-                                                 e4m3x2_to_f16x2(w >> 16));
+                                    uint32_t b0, b1;
+                                    e4m3x4_to_f16x2x2(w, b0, b1);
+                                    mma16816_f16(sc[ks % kQkChains][nt], qa[ks], b0, b1);
                                 }
                         } else {
 #pragma unroll
@@ -521,7 +522,9 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8>::WARPS * 32, 
                             for (int n = 0; n < NT; ++n) {
                                 const uint32_t w =
                                     lds32(vb + n * 128 + ((((lane >> 2) ^ n) & 7) << 4) + 4 * (lane & 3));
-                                mma16816_f16(acc[n], pa, e4m3x2_to_f16x2(w), e4m3x2_to_f16x2(w >> 16));
+                                uint32_t b0, b1;
+                                e4m3x4_to_f16x2x2(w, b0, b1);
+                                mma16816_f16(acc[n], pa, b0, b1);
                             }
                         } else {
                             const int key = (((lane >> 3) & 1) << 3) + (lane & 7);

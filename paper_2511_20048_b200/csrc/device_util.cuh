@@ -112,6 +112,20 @@ __device__ __forceinline__ uint32_t e4m3x2_to_f16x2(uint32_t two_codes) {   // l
     return r;
 }
 
+// Four e4m3 codes (one 4-B fragment load) -> two f16x2 registers: bytes 0,1 -> lo, 2,3 -> hi.
+// The 32-bit word is split into its b16 halves in PTX so ptxas can read the upper half in
+// place instead of shifting it down first.
+__device__ __forceinline__ void e4m3x4_to_f16x2x2(uint32_t w, uint32_t& lo, uint32_t& hi) {
+#if SPA_F8_INTCVT || (defined(SPA_F8_EXP) && SPA_F8_EXP == 2)
+    lo = e4m3x2_to_f16x2(w);
+    hi = e4m3x2_to_f16x2(w >> 16);
+#else
+    asm("{ .reg .b16 l, h; mov.b32 {l, h}, %2; cvt.rn.f16x2.e4m3x2 %0, l; cvt.rn.f16x2.e4m3x2 %1, h; }"
+        : "=r"(lo), "=r"(hi)
+        : "r"(w));
+#endif
+}
+
 __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
     uint32_t v;
     asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
