@@ -15,6 +15,11 @@
 // 128-B-swizzled tiles; the online softmax runs in the log2 domain with lazy rescaling.
 // Each item writes either the final O (bf16) / LSE (fp32) of its rows or an fp32 partial
 // record; partials are merged by the merge kernel (or in-kernel, fused_merge = 1 / 2).
+// F8 = true (S8(f) F4, include/spa.h spa_pool_create_fp8): e4m3 pages, one 4-KB box per
+// page-head (K rows then the transposed V block), f16 MMAs fed by 4-byte fragment loads
+// and cvt.rn.f16x2.e4m3x2; the scales fold into the logit scale and 1/l.
+// DecodeParams::fan (S8(f) F1, spa_decode_attention_fused_gather): every output store also
+// goes to each peer rank's gathered buffer, and the last CTA meets the peers on flags.
 #include <cstdlib>
 
 #include "device_util.cuh"

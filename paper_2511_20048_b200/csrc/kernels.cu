@@ -1,8 +1,9 @@
 // sm_100a kernels of the shared-prefix paged GQA decode-attention step, and their launchers.
 //
 //   append_kernel  a2: scatter new K/V rows of all layers into their (page, slot)
+//   append_f8_kernel  a2 for FP8 pools (S8(f) F4): quantise to e4m3 on the way in
 //   cow_kernel     a3: copy-on-write of a fork's partial last page, all layers
-//   decode_kernel  a5: persistent, one 1-warp (or 2-warp) team per work-item stream:
+//   decode_kernel  a5 (decode.cu): persistent, teams of warps per work-item stream:
 //                  TMA (cp.async.bulk.tensor, 128-B swizzle) page staging into an
 //                  mbarrier ring, ldmatrix + mma.sync bf16 QK^T and PV tiles over all
 //                  R = members x G query rows of a group (so a shared page is read once
