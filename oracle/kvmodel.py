@@ -27,6 +27,11 @@ bit-exactly", BASELINE.json north_star):
   P5  free(req): refcount - 1 on every page of the request, pages reaching 0 return to
       the free set;
   P6  invariant: a page with refcount > 1 is full and is never written again.
+  P7  release_window(reqs, W) (S8(f) F4, ring-buffer storage for sliding-window layers):
+      a query at position q >= len reads keys (q - W, q] (reading #9), so for each listed
+      request the pages i with (i + 1) * ps <= len + 1 - W are dead: refcount - 1 (free at
+      0) and the table entry becomes -1.  A fork copies -1 entries as -1 (no refcount); a
+      fork whose partial page is released is INVALID_ARG.  W <= 0 -> INVALID_ARG.
 
 Status codes mirror include/spa.h: OK 0, INVALID_ARG 1, NO_PAGES 2, BAD_REQUEST 3.
 """
@@ -116,10 +121,13 @@ class PagingModel:
         full, rem = divmod(prefix_len, self.ps)
         if rem and not self._free:
             return NO_PAGES, None
+        if rem and self.tables[parent][full] < 0:
+            return INVALID_ARG, None                            # P7
         st, child = self.alloc()
         shared = self.tables[parent][:full]
         for p in shared:
-            self.refcount[p] += 1
+            if p >= 0:
+                self.refcount[p] += 1
         table = list(shared)
         if rem:
             dst = self._take()
@@ -133,10 +141,27 @@ class PagingModel:
         if req not in self.tables:
             return BAD_REQUEST
         for p in self.tables.pop(req):
+            if p < 0:
+                continue
             self.refcount[p] -= 1
             if self.refcount[p] == 0:
                 heapq.heappush(self._free, p)
         del self.lengths[req]
+        return OK
+
+    def release_window(self, reqs, window: int):
+        if window <= 0:
+            return INVALID_ARG
+        if any(r not in self.tables for r in reqs):
+            return BAD_REQUEST
+        for r in reqs:
+            t = self.tables[r]
+            for i in range(len(t)):
+                if (i + 1) * self.ps <= self.lengths[r] + 1 - window and t[i] >= 0:
+                    self.refcount[t[i]] -= 1
+                    if self.refcount[t[i]] == 0:
+                        heapq.heappush(self._free, t[i])
+                    t[i] = -1
         return OK
 
     def check_invariants(self):
@@ -145,7 +170,8 @@ class PagingModel:
         for r, t in self.tables.items():
             assert len(t) == _cdiv(self.lengths[r], self.ps)
             for i, p in enumerate(t):
-                count[p] += 1
+                if p >= 0:
+                    count[p] += 1
         assert count == self.refcount
         free = set(self._free)
         assert len(free) == len(self._free)
@@ -153,7 +179,7 @@ class PagingModel:
             assert (p in free) == (count[p] == 0)
         for r, t in self.tables.items():
             for i, p in enumerate(t):
-                if self.refcount[p] > 1:
+                if p >= 0 and self.refcount[p] > 1:
                     # shared => full for every holder
                     assert self.lengths[r] >= (i + 1) * self.ps
 

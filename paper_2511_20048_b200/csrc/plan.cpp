@@ -158,7 +158,14 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
     {
         std::unordered_map<int64_t, int> by_key;
         for (int i = 0; i < n_req; ++i) {
-            const int64_t key = P->cfg.sharing ? int64_t(V[i].req->pages[0]) : int64_t(reinterpret_cast<intptr_t>(V[i].req));
+            // the first resident page (pages released by spa_kv_release_window are -1)
+            int64_t first = -1;
+            for (int32_t pg : V[i].req->pages)
+                if (pg >= 0) {
+                    first = pg;
+                    break;
+                }
+            const int64_t key = P->cfg.sharing ? first : int64_t(reinterpret_cast<intptr_t>(V[i].req));
             auto ins = by_key.emplace(key, int(groups.size()));
             if (ins.second) groups.emplace_back();
             groups[ins.first->second].push_back(i);
@@ -218,6 +225,13 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
             }
         }
     }
+
+    // every page a range reads must be resident (spa_kv_release_window leaves -1 entries; a
+    // plan whose window reaches back into them is the caller's error)
+    for (const auto& r : ranges)
+        for (int32_t p = r.a / ps; p < int32_t(cdiv(r.b, ps)); ++p)
+            if ((*r.table)[p] < 0)
+                return fail(SPA_ERR_INVALID_ARG, "plan: a request's window needs a page released by spa_kv_release_window");
 
     // ---- 3. split size
     int64_t total_pages = 0;

@@ -178,10 +178,13 @@ spa_status spa_fork_request(spa_pool* pool, spa_req parent, int32_t prefix_len, 
     const int ps = pool->cfg.page_size;
     const int32_t full = prefix_len / ps, rem = prefix_len % ps;
     if (rem && pool->free_set.empty()) return fail(SPA_ERR_NO_PAGES, "fork: no free page for the partial page copy");
+    if (rem && it->second.pages[full] < 0)
+        return fail(SPA_ERR_INVALID_ARG, "fork: the partial page at the fork point was released (spa_kv_release_window)");
     Request child;
     child.len = prefix_len;
     child.pages.assign(it->second.pages.begin(), it->second.pages.begin() + full);
-    for (int32_t p : child.pages) pool->refcount[p] += 1;
+    for (int32_t p : child.pages)
+        if (p >= 0) pool->refcount[p] += 1;   // released entries (-1) stay released in the child
     int32_t src = -1, dst = -1;
     if (rem) {
         dst = *pool->free_set.begin();
@@ -205,9 +208,32 @@ spa_status spa_kv_free(spa_pool* pool, spa_req req) {
     auto it = pool->reqs.find(req);
     if (it == pool->reqs.end()) return fail(SPA_ERR_BAD_REQUEST, "free: unknown request " + std::to_string(req));
     for (int32_t p : it->second.pages) {
-        if (--pool->refcount[p] == 0) pool->free_set.insert(p);
+        if (p >= 0 && --pool->refcount[p] == 0) pool->free_set.insert(p);
     }
     pool->reqs.erase(it);
+    return SPA_OK;
+}
+
+spa_status spa_kv_release_window(spa_pool* pool, int32_t n_req, const spa_req* reqs, int32_t window) {
+    if (spa_status s = check_pool(pool)) return s;
+    if (window <= 0) return fail(SPA_ERR_INVALID_ARG, "release_window: window must be > 0");
+    if (n_req < 0 || (n_req > 0 && !reqs)) return fail(SPA_ERR_INVALID_ARG, "bad request list");
+    for (int i = 0; i < n_req; ++i)
+        if (pool->reqs.find(reqs[i]) == pool->reqs.end())
+            return fail(SPA_ERR_BAD_REQUEST, "release_window: unknown request " + std::to_string(reqs[i]));
+    const int64_t ps = pool->cfg.page_size;
+    for (int i = 0; i < n_req; ++i) {
+        Request& r = pool->reqs[reqs[i]];
+        // a query at position q >= len reads keys >= q + 1 - window >= len + 1 - window: page p
+        // (keys [p ps, p ps + ps)) is dead once p ps + ps <= len + 1 - window
+        const int64_t dead = std::max<int64_t>(0, (int64_t(r.len) + 1 - window) / ps);
+        for (int64_t p = 0; p < std::min<int64_t>(dead, int64_t(r.pages.size())); ++p) {
+            const int32_t id = r.pages[p];
+            if (id < 0) continue;
+            if (--pool->refcount[id] == 0) pool->free_set.insert(id);
+            r.pages[p] = -1;
+        }
+    }
     return SPA_OK;
 }
 

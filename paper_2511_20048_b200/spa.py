@@ -58,6 +58,7 @@ _SIGS = {
     "spa_kv_append": (c_int32, [c_void_p, c_int32, P_int64, P_int32, c_void_p, c_void_p, c_void_p]),
     "spa_fork_request": (c_int32, [c_void_p, c_int64, c_int32, P_int64, c_void_p]),
     "spa_kv_free": (c_int32, [c_void_p, c_int64]),
+    "spa_kv_release_window": (c_int32, [c_void_p, c_int32, P_int64, c_int32]),
     "spa_kv_page_table": (c_int32, [c_void_p, c_int64, P_int32, c_int32, P_int32, P_int32]),
     "spa_pool_refcounts": (c_int32, [c_void_p, P_int32]),
     "spa_pool_free_pages": (c_int32, [c_void_p, P_int32, c_int32, P_int32]),
@@ -309,6 +310,14 @@ class Pool:
             _check(st)
             return child
         return st, child
+
+    def release_window(self, reqs, window: int, check=True):
+        """spa_kv_release_window: drop the pages no future query can read under `window`."""
+        arr = (c_int64 * max(1, len(reqs)))(*reqs)
+        st = lib().spa_kv_release_window(self.h, len(reqs), arr, int(window))
+        if check:
+            _check(st)
+        return st
 
     def free(self, req, check=True):
         st = spa_kv_free(self.h, req)

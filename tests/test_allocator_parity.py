@@ -96,6 +96,14 @@ class AllocatorMachine(RuleBasedStateMachine):
         rid = data.draw(st.sampled_from(self.ids))
         assert self.pool.free(rid, check=False) == self.model.free(rid)
 
+    @precondition(lambda self: self.ids)
+    @rule(data=st.data())
+    def release_window(self, data):
+        k = data.draw(st.integers(1, 3))
+        reqs = [data.draw(st.sampled_from(self.ids)) for _ in range(k)]
+        w = data.draw(st.sampled_from([0, 1, 15, 16, 17, 40, 100]))
+        assert self.pool.release_window(reqs, w, check=False) == self.model.release_window(reqs, w)
+
     @invariant()
     def same_state(self):
         _state_equal(self.pool, self.model)

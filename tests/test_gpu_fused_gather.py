@@ -12,7 +12,7 @@ north_star tolerances.
 import pytest
 import torch
 
-from harness import LSE_TOL, O_TOL, GpuBatch, bits_to_torch, compare
+from harness import LSE_TOL, O_TOL, GpuBatch, bits_to_torch, compare, fp8_scales
 from oracle.replay import Replay
 from paper_2511_20048_b200 import spa
 from spa_inputs import families, workloads
@@ -34,8 +34,8 @@ def _inputs(seed=3, layers=2):
     return rec, families.make_inputs(rec, "needle_shared_pos")
 
 
-def _shards(inp, n, merge_mode):
-    shards = [GpuBatch(inp, shard=(r, n)) for r in range(n)]
+def _shards(inp, n, merge_mode, kv_scale=None):
+    shards = [GpuBatch(inp, shard=(r, n), kv_scale=kv_scale) for r in range(n)]
     plans = []
     for gb in shards:
         p = spa.Plan(gb.pool, split_pages=5, num_ctas=3, merge_mode=merge_mode)
@@ -110,3 +110,38 @@ def test_fused_gather_without_lse_and_rejections():
         o, _ = peers[r].views(0, N, Hq, d)
         assert torch.equal(o.permute(1, 0, 2), torch.cat([ref[0][0], ref[1][0]], dim=1))
         assert peers[r].status() == 0
+
+
+@pytest.mark.timeout(300, method="thread")
+def test_fused_gather_fp8_pages_bitwise():
+    """F1 x F4: head-sharded FP8 pools, fused gather == the unsharded FP8 decode, bitwise."""
+    rec, inp = _inputs(seed=6)
+    sc = fp8_scales(inp)
+    full = GpuBatch(inp, kv_scale=sc)
+    plan = spa.Plan(full.pool, split_pages=5, num_ctas=7)
+    plan.plan(full.reqs)
+    refs = [full.decode(plan, li) for li in range(2)]
+    N, Hq, d = refs[0][0].shape
+    n = 4
+    shards, plans = _shards(inp, n, 0, kv_scale=sc)
+    peers = spa.Peer.local_world(n, spa.Peer.buffer_bytes(N, Hq, d), n_bufs=2)
+    streams = [torch.cuda.Stream() for _ in range(n)]
+    qs = [[bits_to_torch(inp.q[li][:, gb.q_sl]).contiguous() for gb in shards] for li in range(2)]
+    torch.cuda.synchronize()
+    for step in range(2):
+        for r in range(n):
+            peers[r].decode(plans[r], step, qs[step][r], buf_idx=step, scale=rec.model.softmax_scale,
+                            stream=streams[r])
+    torch.cuda.synchronize()
+    rp = Replay(inp, kv_fp8_scale=sc)
+    for r in range(n):
+        assert peers[r].status() == 0
+        for b in range(2):
+            o, lse = peers[r].views(b, N, Hq, d)
+            assert torch.equal(o.permute(1, 0, 2), refs[b][0]) and torch.equal(lse.t(), refs[b][1])
+    O_ref, L_ref = rp.expected(1, inp.q[1])
+    o, lse = peers[0].views(1, N, Hq, d)
+    eo, el = compare(o.permute(1, 0, 2), lse.t(), O_ref, L_ref)
+    assert eo <= O_TOL and el <= LSE_TOL, (eo, el)
+    for p in peers:
+        p.close()

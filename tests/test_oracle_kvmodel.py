@@ -165,3 +165,39 @@ def test_zero_and_full_prefix_forks():
     st1, c1 = m.fork(a, 6)
     assert st1 == OK and m.page_table(c1)[1] == [0, 2] and m.cow_log[-1] == (1, 2, 2)
     m.check_invariants()
+
+
+def test_release_window_rule_by_brute_force():
+    """P7 pinned by its definition (reading #9): after release_window(W) at length n, every
+    key a future query (position q >= n, keys (q - W, q]) can read lies in a resident page,
+    and every released page holds only keys < n + 1 - W."""
+    for n in range(0, 90, 7):
+        for W in (1, 2, 15, 16, 17, 31, 32, 33, 64, 200):
+            m = PagingModel(20, 16)
+            _, r = m.alloc()
+            assert m.append([r], [n]) == 0
+            assert m.release_window([r], W) == 0
+            t = m.tables[r]
+            for q in range(n, n + 40):                 # future queries (after more appends)
+                for key in range(max(0, q + 1 - W), min(q + 1, n)):
+                    assert t[key // 16] >= 0, (n, W, q, key)
+            for i, p in enumerate(t):
+                if p < 0:
+                    assert (i + 1) * 16 <= n + 1 - W
+            m.check_invariants()
+
+
+def test_release_window_hand_case_and_forks():
+    m = PagingModel(20, 16)
+    _, r = m.alloc()
+    m.append([r], [100])                               # pages 0..6, keys 0..99
+    assert m.release_window([r], 32) == 0              # a query at 100 reads keys 69..100
+    assert m.tables[r] == [-1, -1, -1, -1, 4, 5, 6]    # pages 0-3 hold keys 0..63 only
+    assert m.free_pages == list(range(0, 4)) + list(range(7, 20))
+    st, c = m.fork(r, 96)                              # full pages only: -1 entries copied
+    assert st == 0 and m.tables[c] == [-1, -1, -1, -1, 4, 5]
+    assert m.refcount[4] == m.refcount[5] == 2 and m.refcount[6] == 1
+    assert m.fork(r, 40)[0] == 1                       # partial page 2 was released
+    assert m.release_window([r], 0) == 1 and m.release_window([999], 5) == 3
+    assert m.free(c) == 0 and m.refcount[4] == 1
+    m.check_invariants()

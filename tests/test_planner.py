@@ -232,3 +232,34 @@ def test_extend_plan_errors():
         assert e.value.status == spa.SPA_ERR_INVALID_ARG
     plan.plan([a], n_query=[5])
     assert plan.stats()["n_req"] == 5
+
+
+def test_window_release_bounds_a_local_layer_pool():
+    """F4 ring buffer, host side: a Gemma-shaped local-layer pool (W = 1024) that releases
+    after every decode step holds about W/16 + 2 pages per request instead of len/16."""
+    from spa_inputs import workloads as wl
+
+    rec = wl.gemma(seed=2, n_agents=8)
+    pool = spa.Pool(1, 32, 16, 128, 40000)                 # metadata only
+    ops, batch = wl.call_log(rec)
+    ids = {}
+    for op in ops:
+        if op[0] == "alloc":
+            ids[op[1]] = pool.alloc()
+        elif op[0] == "append":
+            pool.append([ids[op[1]]], [op[4]])
+        elif op[0] == "fork":
+            ids[op[1]] = pool.fork(ids[op[2]], op[3])
+    reqs = [ids[n] for n in batch]
+    used_full = pool.num_pages - len(pool.free_pages())
+    W = 1024
+    pool.release_window(list(ids.values()), W + 1)
+    for _ in range(40):
+        pool.append(reqs, [1] * len(reqs))
+        pool.release_window(list(ids.values()), W + 1)
+        plan = spa.Plan(pool)
+        plan.plan(reqs, W)
+    used = pool.num_pages - len(pool.free_pages())
+    resident = [sum(p >= 0 for p in pool.page_table(i)[1]) for i in ids.values()]
+    assert max(resident) <= W // 16 + 2
+    assert used < used_full / 4
