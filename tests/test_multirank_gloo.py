@@ -61,6 +61,13 @@ def _worker(rank, world, port, q):
         plan.plan(reqs)
         digests = [None] * world
         dist.all_gather_object(digests, _state_digest(pool, plan, reqs))
+        # a windowed (local-layer) step after spa_kv_release_window replicates as well
+        pool.release_window(list(ids.values()), 1025)
+        pool.append(reqs, [1] * len(reqs))
+        plan.plan(reqs, 1024)
+        wdig = [None] * world
+        dist.all_gather_object(wdig, _state_digest(pool, plan, reqs))
+        digests = [a + b for a, b in zip(digests, wdig)]
         uid = [os.urandom(128) if rank == 0 else None]   # stands in for spa_nccl_unique_id()
         dist.broadcast_object_list(uid, src=0)
         uids = [None] * world
