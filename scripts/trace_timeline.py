@@ -134,6 +134,7 @@ def main():
     ap.add_argument("--split", type=int, default=0)
     ap.add_argument("--merge", type=int, default=0)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--kv", default="bf16", choices=["bf16", "fp8"])
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     stream = torch.cuda.Stream()
@@ -147,7 +148,9 @@ def main():
         rec = workloads.sweep(int(b), float(f))
     m = rec.model
     Lr = 8 if a.workload != "long" else 2
-    pool = spa.Pool(Lr, m.num_q_heads, m.num_kv_heads, m.head_dim, bench.pages_for(rec, 8), device=dev)
+    fp8 = a.kv == "fp8"
+    pool = spa.Pool(Lr, m.num_q_heads, m.num_kv_heads, m.head_dim, bench.pages_for(rec, 8), device=dev,
+                    kv_scale=np.full((Lr, m.num_kv_heads, 2), bench.FP8_SCALE, np.float32) if fp8 else None)
     ids, reqs, batch = bench.build_batch(spa, pool, rec, list(range(Lr)), slice(0, m.num_kv_heads), dev, fill="reuse")
     N = len(reqs)
     q = kv_bits_torch(rec.seed, KIND_Q, 1, list(range(Lr)), np.arange(N), m.num_q_heads, m.head_dim, dev).contiguous()
@@ -196,7 +199,7 @@ def main():
     torch.cuda.synchronize()
     res = {"workload": a.workload, "N": N, "stats": st, "eager_chained_us": eager_us,
            "graph_chained_us": float(np.median(graph_us)), "host_us_per_call": host_us,
-           "alg_bytes": bench.alg_bytes(st, N, m.num_kv_heads, m.num_q_heads, m.head_dim)}
+           "alg_bytes": bench.alg_bytes(st, N, m.num_kv_heads, m.num_q_heads, m.head_dim, 1 if fp8 else 2), "kv": a.kv}
     res["trace"] = analyse(buf)
     descs = plan.debug_array(0)
     items = plan.debug_array(2)
