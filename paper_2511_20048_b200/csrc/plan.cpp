@@ -152,21 +152,51 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
     std::vector<int32_t> lo(n_req);
     for (int i = 0; i < n_req; ++i) lo[i] = window > 0 ? std::max<int32_t>(0, V[i].hi - window) : 0;
 
-    // ---- 1. groups (first page id; sharing off: each request alone), then sub-groups of at
-    //      most max_rows / G rows (the rows of a request stay consecutive)
+    // ---- 1. groups (requests that share page ids; sharing off: each request alone), then
+    //      sub-groups of at most max_rows / G rows (the rows of a request stay consecutive).
+    //      Page ids are positional (a shared page sits at the same index in every table
+    //      holding it).  Without released pages this is "same first page"; after
+    //      spa_kv_release_window the members of a family may have released different
+    //      leading pages, so requests are joined when one of a request's first kLinkPages
+    //      resident pages is held by another.
+    std::vector<int32_t> d(n_req, 0);   // index of the first resident page
+    for (int i = 0; i < n_req; ++i) {
+        const auto& t = V[i].req->pages;
+        while (d[i] < int32_t(t.size()) && t[d[i]] < 0) ++d[i];
+    }
     std::vector<std::vector<int>> groups;
     {
-        std::unordered_map<int64_t, int> by_key;
-        for (int i = 0; i < n_req; ++i) {
-            // the first resident page (pages released by spa_kv_release_window are -1)
-            int64_t first = -1;
-            for (int32_t pg : V[i].req->pages)
-                if (pg >= 0) {
-                    first = pg;
-                    break;
+        std::vector<int> parent(n_req);
+        for (int i = 0; i < n_req; ++i) parent[i] = i;
+        auto find = [&](int x) {
+            while (parent[x] != x) x = parent[x] = parent[parent[x]];
+            return x;
+        };
+        if (P->cfg.sharing) {
+            constexpr int32_t kLinkPages = 64;
+            std::unordered_map<int32_t, int> holder;
+            for (int i = 0; i < n_req; ++i) {
+                const auto& t = V[i].req->pages;
+                const int32_t e = std::min<int32_t>(int32_t(t.size()), d[i] + kLinkPages);
+                for (int32_t k = d[i]; k < e; ++k) {
+                    auto ins = holder.emplace(t[k], i);
+                    if (!ins.second) {   // another request holds this page: same family
+                        const int a = find(i), b = find(ins.first->second);
+                        if (a != b) parent[std::max(a, b)] = std::min(a, b);
+                    }
                 }
-            const int64_t key = P->cfg.sharing ? first : int64_t(reinterpret_cast<intptr_t>(V[i].req));
-            auto ins = by_key.emplace(key, int(groups.size()));
+            }
+        } else {
+            // rows of one request (extend) stay together
+            std::unordered_map<const Request*, int> first;
+            for (int i = 0; i < n_req; ++i) {
+                auto ins = first.emplace(V[i].req, i);
+                if (!ins.second) parent[i] = ins.first->second;
+            }
+        }
+        std::unordered_map<int, int> gi;
+        for (int i = 0; i < n_req; ++i) {
+            auto ins = gi.emplace(find(i), int(groups.size()));
             if (ins.second) groups.emplace_back();
             groups[ins.first->second].push_back(i);
         }
@@ -183,12 +213,15 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
         for (size_t s0 = 0; s0 < grp.size(); s0 += max_members) {
             std::vector<int> sg(grp.begin() + s0, grp.begin() + std::min(grp.size(), s0 + max_members));
             const int gid = n_groups++;
-            int32_t cp = 0;
+            // common page-id run [start, cp) of the sub-group: start = the first index every
+            // member holds (0 unless pages were released), S = cp * ps
+            int32_t cp = 0, start = 0;
             bool one_table = true;
             for (int m : sg) one_table &= V[m].req == V[sg[0]].req;
             if (sg.size() > 1 && !one_table) {
+                for (int m : sg) start = std::max(start, d[m]);
                 const auto& t0 = V[sg[0]].req->pages;
-                for (;; ++cp) {
+                for (cp = start;; ++cp) {
                     bool ok = true;
                     for (int m : sg) {
                         const auto& t = V[m].req->pages;
@@ -196,14 +229,34 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
                     }
                     if (!ok) break;
                 }
+                if (cp == start) cp = start = 0;   // nothing in common: every member reads its own range
             }
-            const int32_t S = cp * ps;
-            if (S > 0) {
+            const int32_t S = cp * ps, S0 = start * ps;
+            if (S > S0) {
                 std::vector<int> shared;
                 int32_t lo_min = S;
                 for (int m : sg)
                     if (lo[m] < S) { shared.push_back(m); lo_min = std::min(lo_min, lo[m]); }
-                if (!shared.empty()) ranges.push_back(Range{0, gid, shared, lo_min, S, &V[sg[0]].req->pages});
+                if (!shared.empty())
+                    ranges.push_back(Range{0, gid, shared, std::max(lo_min, S0), S, &V[sg[0]].req->pages});
+                // keys below the common run (a member that released fewer leading pages than
+                // another): read from the member's own table
+                for (size_t k = 0; k < sg.size();) {
+                    size_t e = k;
+                    while (e < sg.size() && V[sg[e]].req == V[sg[k]].req) ++e;
+                    std::vector<int> mem;
+                    int32_t a = INT32_MAX, b = 0;
+                    for (size_t x = k; x < e; ++x) {
+                        const int m = sg[x];
+                        if (lo[m] < S0) {
+                            mem.push_back(m);
+                            a = std::min(a, lo[m]);
+                            b = std::max(b, std::min(S0, V[m].hi));
+                        }
+                    }
+                    if (!mem.empty() && a < b) ranges.push_back(Range{1, gid, mem, a, b, &V[sg[k]].req->pages});
+                    k = e;
+                }
             }
             // per request (page table): its rows' keys beyond S
             for (size_t k = 0; k < sg.size();) {

@@ -52,3 +52,26 @@ def test_windowed_decode_after_release(family):
     z = bits_to_torch(np.zeros((1, 16 * free_before, 4, 128), np.uint16))
     gb.pool.append([a], [16 * free_before], z, z)
     assert len(gb.pool.free_pages()) == 0
+
+
+@pytest.mark.parametrize("family", ["needle_shared_pos", "needle_tail_pos", "flat"])
+def test_released_family_shares_and_matches_oracle(family):
+    """A parent and 3 forks release different leading pages; the plan still reads their
+    common window region once (plus a head range) and decode matches the oracle."""
+    W = 200
+    model = workloads.Model("m", 1, 16, 4, 128)
+    rec = workloads.Recipe("fam", model, [workloads.Group(600, 5, [20, 25, 30]),
+                                          workloads.Group(333, 40, [17, 19])], seed=12)
+    inp = families.make_inputs(rec, family)
+    gb = GpuBatch(inp, num_pages=200)
+    gb.pool.release_window(list(gb.ids.values()), W + 1)
+    rp = Replay(inp)
+    for split in (0, 3):
+        plan = spa.Plan(gb.pool, split_pages=split)
+        plan.plan(gb.reqs, W)
+        st = plan.stats()
+        assert st["n_groups"] == 2 and st["unique_tokens"] < st["unshared_tokens"]
+        o, lse = gb.decode(plan, 0)
+        O, L = rp.expected(0, inp.q[0], window=W)
+        eo, el = compare(o, lse, O, L)
+        assert eo <= O_TOL and el <= LSE_TOL, (split, eo, el)

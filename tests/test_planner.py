@@ -263,3 +263,43 @@ def test_window_release_bounds_a_local_layer_pool():
     resident = [sum(p >= 0 for p in pool.page_table(i)[1]) for i in ids.values()]
     assert max(resident) <= W // 16 + 2
     assert used < used_full / 4
+
+
+def test_release_keeps_prefix_sharing_within_a_family():
+    """After spa_kv_release_window a parent and its forks release different leading pages
+    (their lengths differ); the planner still groups them and reads their common window
+    region once, plus a small head range for the member whose window starts earlier."""
+    pool = spa.Pool(1, 8, 2, 128, 400)
+    parent = pool.alloc()
+    pool.append([parent], [600])
+    forks = [pool.fork(parent, 600) for _ in range(3)]
+    pool.append(forks, [20, 25, 30])
+    pool.append([parent], [5])
+    reqs = [parent] + forks
+    W = 200
+    pool.release_window(reqs, W + 1)
+    assert len({pool.page_table(r)[1].count(-1) for r in reqs}) > 1     # different release points
+    on, off = spa.Plan(pool), spa.Plan(pool, sharing=False)
+    on.plan(reqs, W)
+    off.plan(reqs, W)
+    s_on, s_off = on.stats(), off.stats()
+    assert s_on["n_groups"] == 1 and s_off["n_groups"] == 4
+    assert s_on["unshared_tokens"] == s_off["unique_tokens"] == 4 * W
+    # the common region [max first resident key, 600) is read once instead of 4 times
+    assert s_on["unique_tokens"] < 0.5 * s_off["unique_tokens"]
+
+
+def test_release_family_grouping_with_parent_first_in_batch():
+    """The parent (listed first, longest) releases the most pages; forks link to it through
+    the pages they still share."""
+    pool = spa.Pool(1, 8, 2, 128, 200)
+    parent = pool.alloc()
+    pool.append([parent], [333])
+    forks = [pool.fork(parent, 333) for _ in range(2)]
+    pool.append(forks, [17, 19])
+    pool.append([parent], [40])
+    reqs = [parent] + forks
+    pool.release_window(reqs, 201)
+    plan = spa.Plan(pool)
+    plan.plan(reqs, 200)
+    assert plan.stats()["n_groups"] == 1
