@@ -1,4 +1,4 @@
-"""Full-size parity: BASELINE.json configs 1 and 2 at their bench sizes, in the launch
+"""Full-size parity: BASELINE.json configs 1 and 2 at their bench sizes (bf16, and FP8 pages), in the launch
 configuration bench.py times (persistent grid, automatic splits, in-kernel tail merge,
 PDL-chained layer calls), checked on sampled outputs the fp64 oracle computes one by one.
 """
@@ -13,7 +13,7 @@ from spa_inputs import KIND_K, KIND_Q, KIND_V, kv_bits_np, kv_bits_torch
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 
-def _run(config, resident, sample_groups, calls_to_check):
+def _run(config, resident, sample_groups, calls_to_check, fp8=False):
     recipe = bench.recipe_for(config)
     m = recipe.model
     dev = torch.device("cuda", 0)
@@ -21,7 +21,8 @@ def _run(config, resident, sample_groups, calls_to_check):
     torch.cuda.set_stream(stream)
     layers = list(range(resident))
     sched = bench.layer_schedule(recipe, resident)
-    pool = spa.Pool(resident, m.num_q_heads, m.num_kv_heads, m.head_dim, bench.pages_for(recipe, 4), device=dev)
+    pool = spa.Pool(resident, m.num_q_heads, m.num_kv_heads, m.head_dim, bench.pages_for(recipe, 4), device=dev,
+                    kv_scale=np.full((resident, m.num_kv_heads, 2), bench.FP8_SCALE, np.float32) if fp8 else None)
     ids, reqs, batch = bench.build_batch(spa, pool, recipe, layers, slice(0, m.num_kv_heads), dev)
     N = len(reqs)
     # one decode step: append the step token, plan every window, run the whole schedule chained
@@ -44,7 +45,7 @@ def _run(config, resident, sample_groups, calls_to_check):
     for ci in calls_to_check:
         r, w = sched[ci]
         qb = kv_bits_np(recipe.seed, KIND_Q, 1_000_000, [r], np.arange(N), m.num_q_heads, m.head_dim)[0]
-        O, L = bench.oracle_sample(recipe, batch, rows, r, qb, steps_appended=1, window=w)
+        O, L = bench.oracle_sample(recipe, batch, rows, r, qb, steps_appended=1, window=w, fp8=fp8)
         eo = float(np.abs(o[ci, rows].float().cpu().numpy() - O).max())
         el = float(np.abs(lse[ci, rows].cpu().numpy() - L).max())
         worst = (max(worst[0], eo), max(worst[1], el))
@@ -58,4 +59,14 @@ def test_qwen_config_full_size_sampled():
 
 def test_gemma_config_full_size_sampled():
     eo, el = _run("gemma", 6, {0, 40}, [0, 5, 61])       # local, global, local
+    assert eo <= 2e-2 and el <= 1e-3, (eo, el)
+
+
+def test_qwen_config_full_size_sampled_fp8_pages():
+    eo, el = _run("qwen", 64, {0, 31}, [0, 63], fp8=True)
+    assert eo <= 2e-2 and el <= 1e-3, (eo, el)
+
+
+def test_gemma_config_full_size_sampled_fp8_pages():
+    eo, el = _run("gemma", 6, {0, 40}, [0, 5], fp8=True)
     assert eo <= 2e-2 and el <= 1e-3, (eo, el)
