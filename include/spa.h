@@ -127,13 +127,15 @@ spa_status spa_fork_request(spa_pool* pool, spa_req parent, int32_t prefix_len, 
 spa_status spa_kv_free(spa_pool* pool, spa_req req);
 
 /* F4 (ring-buffer storage for sliding-window layers): release the
- * pages no future query of reqs[i] can read under a sliding window of `window` tokens
- * (reading #9: a query at position q reads keys (q - window, q]).  Queries come at
- * positions >= the current length n, so page p (keys [16p, 16p + 16)) is released when
- * 16p + 16 <= n + 1 - window: its refcount drops, at 0 it returns to the free set, and the
- * request's page-table entry becomes -1 (lengths and later entries are unchanged).  For a
- * pool that holds only windowed (local) layers, calling this after every append bounds
- * each request to about window/16 + 1 pages.  Host only.  Errors: window <= 0,
+ * pages neither the current query nor any later query of reqs[i] can read under a sliding
+ * window of `window` tokens (reading #9: a query at position q reads keys (q - window, q]).
+ * Under append-then-attend (reading #8) the current step's query is the last appended
+ * token, at position n - 1 for the current length n, so page p (keys [16p, 16p + 16)) is
+ * released when 16p + 16 <= n - window: its refcount drops, at 0 it returns to the free
+ * set, and the request's page-table entry becomes -1 (lengths and later entries are
+ * unchanged).  Intended order per step: spa_kv_append, spa_kv_release_window(window),
+ * spa_decode_plan(window).  For a pool that holds only windowed (local) layers this bounds
+ * each request to about window/16 + 2 pages.  Host only.  Errors: window <= 0,
  * unknown request; later, a plan whose window reaches a released page (INVALID_ARG) and
  * a fork whose partial page was released (INVALID_ARG).  Forks copy released entries as -1. */
 spa_status spa_kv_release_window(spa_pool* pool, int32_t n_req, const spa_req* reqs, int32_t window);

@@ -28,9 +28,10 @@ bit-exactly", BASELINE.json north_star):
       the free set;
   P6  invariant: a page with refcount > 1 is full and is never written again.
   P7  release_window(reqs, W) (S8(f) F4, ring-buffer storage for sliding-window layers):
-      a query at position q >= len reads keys (q - W, q] (reading #9), so for each listed
-      request the pages i with (i + 1) * ps <= len + 1 - W are dead: refcount - 1 (free at
-      0) and the table entry becomes -1.  A fork copies -1 entries as -1 (no refcount); a
+      under append-then-attend (reading #8) the current step's query sits at len - 1 and
+      later ones after it; a query at q reads keys (q - W, q] (reading #9), so for each
+      listed request the pages i with (i + 1) * ps <= len - W are dead: refcount - 1
+      (free at 0) and the table entry becomes -1.  A fork copies -1 entries as -1 (no refcount); a
       fork whose partial page is released is INVALID_ARG.  W <= 0 -> INVALID_ARG.
 
 Status codes mirror include/spa.h: OK 0, INVALID_ARG 1, NO_PAGES 2, BAD_REQUEST 3.
@@ -157,7 +158,7 @@ class PagingModel:
         for r in reqs:
             t = self.tables[r]
             for i in range(len(t)):
-                if (i + 1) * self.ps <= self.lengths[r] + 1 - window and t[i] >= 0:
+                if (i + 1) * self.ps <= self.lengths[r] - window and t[i] >= 0:
                     self.refcount[t[i]] -= 1
                     if self.refcount[t[i]] == 0:
                         heapq.heappush(self._free, t[i])

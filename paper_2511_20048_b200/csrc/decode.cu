@@ -706,7 +706,7 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8>::WARPS * 32, 
             t = __shfl_sync(0xffffffffu, t, 0);
             if (t >= n_sub) break;
             const int code = msub[t];
-            const int task = code >> 6, sub = code & 63;
+            const int task = code >> 8, sub = code & 255;
             tr(4, t);
             const int row = task / Hkv, g = task - row * Hkv;
             const int s0 = rec_ptr[row], s1 = rec_ptr[row + 1];
@@ -764,13 +764,8 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8>::WARPS * 32, 
 template <int D, int MT, int PPS, int TEAMS, bool F8 = false>
 static int launch_decode_t(const spa_plan* P, const DecodeParams& dp, void* stream) {
     using C = DecodeCfg<D, MT, PPS, TEAMS, F8>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(decode_kernel<D, MT, PPS, TEAMS, F8>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-        if (e) return int(e);
-        attr_set = true;
-    }
+    static std::atomic<unsigned long long> attr_done{0};
+    if (int e = set_smem_attr_once(decode_kernel<D, MT, PPS, TEAMS, F8>, C::SMEM, &attr_done)) return e;
     const CUtensorMap* tk = reinterpret_cast<const CUtensorMap*>(P->pool->tmap_k.bytes);
     const CUtensorMap* tv = reinterpret_cast<const CUtensorMap*>(P->pool->tmap_v.bytes);
     return launch_pdl(decode_kernel<D, MT, PPS, TEAMS, F8>, dim3(P->num_ctas), dim3(C::WARPS * 32), C::SMEM, stream,

@@ -1,6 +1,8 @@
 // Device helpers shared by the sm_100a kernels (PTX wrappers: mbarrier, TMA, ldmatrix,
 // mma.sync, scoped atomics) and the PDL launch helper.
 #pragma once
+
+#include <atomic>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -229,6 +231,21 @@ static int launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sm
     cfg.attrs = attr;
     cfg.numAttrs = no_pdl ? 0 : 1;
     return int(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device context: remember it per
+// device (bit d of *done), so a process driving several devices raises the limit on each.
+template <typename... KArgs>
+static int set_smem_attr_once(void (*kernel)(KArgs...), int smem, std::atomic<unsigned long long>* done) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e) return int(e);
+    const unsigned long long bit = dev < 64 ? 1ull << dev : 0ull;
+    if (bit && (done->load(std::memory_order_acquire) & bit)) return 0;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e) return int(e);
+    done->fetch_or(bit, std::memory_order_acq_rel);
+    return 0;
 }
 
 // Merge the split partials of G <= 8 consecutive heads [head0, head0 + G) of one request

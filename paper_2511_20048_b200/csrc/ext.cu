@@ -554,12 +554,8 @@ int launch_ext(const spa_plan* P, int32_t layer, const void* q, int64_t q_sr, in
     const auto& c = P->pool->cfg;
     const int32_t* H = P->host.data();
     if (H[H_N_ITEMS] == 0) return 0;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(ext_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ext::SMEM);
-        if (e) return int(e);
-        attr_set = true;
-    }
+    static std::atomic<unsigned long long> attr_done{0};
+    if (int e = set_smem_attr_once(ext_kernel, ext::SMEM, &attr_done)) return e;
     // 16-B vector loads of q rows and stores of o rows
     if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(o)) % 16 || q_sr % 8 || q_sh % 8 || o_sr % 8 ||
         o_sh % 8)

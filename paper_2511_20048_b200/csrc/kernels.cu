@@ -35,6 +35,11 @@ int device_sm_count(int* dev_out) {
     return sms;
 }
 
+int current_device() {
+    int dev = -1;
+    return cudaGetDevice(&dev) == cudaSuccess ? dev : -1;
+}
+
 const char* cuda_error_string(int err) { return cudaGetErrorString(cudaError_t(err)); }
 
 static size_t pool_bytes(const spa_pool* p) {

@@ -119,6 +119,7 @@ spa_status spa_extend_plan(spa_plan* P, int32_t n_req, const spa_req* reqs, cons
                            void* stream) {
     if (!P) return fail(SPA_ERR_INVALID_ARG, "null plan");
     spa_pool* pool = P->pool;
+    if (spa_status s = check_device(pool)) return s;
     if (n_req < 0 || (n_req > 0 && !reqs)) return fail(SPA_ERR_INVALID_ARG, "bad request list");
     std::vector<VRow> V;
     V.reserve(size_t(n_req));
@@ -173,13 +174,20 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
             return x;
         };
         if (P->cfg.sharing) {
-            constexpr int32_t kLinkPages = 64;
+            // Sharing is positional and prefix-shaped (a fork shares its parent's first pages,
+            // spa_kv_release_window drops a prefix), so two requests share a resident page iff
+            // they hold the same page at index max(d_i, d_j).  Probing every request at every
+            // distinct first-resident index D (one index, 0, without releases) finds exactly
+            // those pairs: O(N |D|) hash probes instead of one per resident page.
+            std::vector<int32_t> D(d.begin(), d.end());
+            std::sort(D.begin(), D.end());
+            D.erase(std::unique(D.begin(), D.end()), D.end());
             std::unordered_map<int32_t, int> holder;
+            holder.reserve(size_t(n_req) * 2);
             for (int i = 0; i < n_req; ++i) {
                 const auto& t = V[i].req->pages;
-                const int32_t e = std::min<int32_t>(int32_t(t.size()), d[i] + kLinkPages);
-                for (int32_t k = d[i]; k < e; ++k) {
-                    auto ins = holder.emplace(t[k], i);
+                for (auto k = std::lower_bound(D.begin(), D.end(), d[i]); k != D.end() && *k < int32_t(t.size()); ++k) {
+                    auto ins = holder.emplace(t[*k], i);
                     if (!ins.second) {   // another request holds this page: same family
                         const int a = find(i), b = find(ins.first->second);
                         if (a != b) parent[std::max(a, b)] = std::min(a, b);
@@ -447,9 +455,9 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
         for (int32_t t = 0; t < int32_t(last.size()); ++t)
             if (last[t] >= 0) tasks.push_back(t);
         std::stable_sort(tasks.begin(), tasks.end(), [&](int32_t a, int32_t b) { return last[a] < last[b]; });
-        // subtask codes: task * 64 + 1 + hh (head hh alone: the heads of a task merge in
-        // parallel, ~one L2 round trip after its last record) or, when there are many more
-        // head merges than warps, task * 64 + 0 (one warp merges all G heads of the task with
+        // subtask codes: task * 256 + 1 + hh (head hh alone: the heads of a task merge in
+        // parallel, ~one L2 round trip after its last record; G <= max_rows <= 128 < 255) or,
+        // when there are many more head merges than warps, task * 256 + 0 (one warp merges all G heads of the task with
         // their loads in flight together: fewer, longer subtasks; needs G x S <= 32)
         const int64_t warps_total = int64_t(P->num_ctas) * P->teams * P->mt * 2;
         bool whole = int64_t(tasks.size()) * G > 4 * warps_total;
@@ -457,9 +465,9 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
         for (int32_t t : tasks) {
             const int32_t S = rec_ptr[t / Hkv + 1] - rec_ptr[t / Hkv];
             if (whole && G <= 8 && G * S <= 32 && S <= 16) {
-                mtask.push_back(t * 64);
+                mtask.push_back(t * 256);
             } else {
-                for (int hh = 0; hh < G; ++hh) mtask.push_back(t * 64 + 1 + hh);
+                for (int hh = 0; hh < G; ++hh) mtask.push_back(t * 256 + 1 + hh);
             }
         }
     }

@@ -33,6 +33,17 @@ static spa_status check_pool(const spa_pool* p) {
     return SPA_OK;
 }
 
+// Device work of a pool is launched on the calling thread's current device, which must be
+// the device the pool was created on (its tensor maps and kernel attributes live there).
+spa_status check_device(const spa_pool* p) {
+    if (p->metadata_only) return SPA_OK;
+    const int dev = current_device();
+    if (dev != p->device)
+        return fail(SPA_ERR_INVALID_ARG, "the current CUDA device (" + std::to_string(dev) +
+                                             ") is not the pool's device (" + std::to_string(p->device) + ")");
+    return SPA_OK;
+}
+
 }  // namespace spa
 
 using namespace spa;
@@ -127,6 +138,7 @@ spa_status spa_kv_alloc(spa_pool* pool, spa_req* out_req) {
 spa_status spa_kv_append(spa_pool* pool, int32_t n_req, const spa_req* reqs, const int32_t* n_new,
                          const void* k_new, const void* v_new, void* stream) {
     if (spa_status s = check_pool(pool)) return s;
+    if (spa_status s = check_device(pool)) return s;
     if (n_req < 0 || (n_req > 0 && (!reqs || !n_new))) return fail(SPA_ERR_INVALID_ARG, "bad request list");
     const int ps = pool->cfg.page_size;
     std::unordered_set<int64_t> seen;
@@ -170,6 +182,7 @@ spa_status spa_kv_append(spa_pool* pool, int32_t n_req, const spa_req* reqs, con
 
 spa_status spa_fork_request(spa_pool* pool, spa_req parent, int32_t prefix_len, spa_req* out_child, void* stream) {
     if (spa_status s = check_pool(pool)) return s;
+    if (spa_status s = check_device(pool)) return s;
     if (!out_child) return fail(SPA_ERR_INVALID_ARG, "null out_child");
     auto it = pool->reqs.find(parent);
     if (it == pool->reqs.end()) return fail(SPA_ERR_BAD_REQUEST, "fork: unknown parent " + std::to_string(parent));
@@ -224,9 +237,10 @@ spa_status spa_kv_release_window(spa_pool* pool, int32_t n_req, const spa_req* r
     const int64_t ps = pool->cfg.page_size;
     for (int i = 0; i < n_req; ++i) {
         Request& r = pool->reqs[reqs[i]];
-        // a query at position q >= len reads keys >= q + 1 - window >= len + 1 - window: page p
-        // (keys [p ps, p ps + ps)) is dead once p ps + ps <= len + 1 - window
-        const int64_t dead = std::max<int64_t>(0, (int64_t(r.len) + 1 - window) / ps);
+        // append-then-attend (reading #8): the current step's query sits at len - 1 and reads
+        // keys >= len - window, later queries only later keys, so page p (keys [p ps, p ps +
+        // ps)) is dead once p ps + ps <= len - window
+        const int64_t dead = std::max<int64_t>(0, (int64_t(r.len) - window) / ps);
         for (int64_t p = 0; p < std::min<int64_t>(dead, int64_t(r.pages.size())); ++p) {
             const int32_t id = r.pages[p];
             if (id < 0) continue;

@@ -37,7 +37,7 @@ enum MetaHeader : int {
     H_N_PAGES = 14,
     H_OFF_COUNTERS = 15,   // int32 [n_req][Hkv] record arrivals of the in-kernel merges (launch k of a plan
                            // completes a task at (k + 1) x its records; zeroed by the plan upload)
-    H_OFF_MTASK = 16,      // int32 [n_mtask]: tail-merge subtasks (row * Hkv + kv_head) * 64 + (0: all G
+    H_OFF_MTASK = 16,      // int32 [n_mtask]: tail-merge subtasks (row * Hkv + kv_head) * 256 + (0: all G
                            // heads | 1 + head), earliest-ready first
     H_N_MTASK = 17,
     H_WORDS = 20
@@ -186,5 +186,7 @@ int launch_ext(const spa_plan* plan, int32_t layer, const void* q, int64_t q_sr,
 int memset_pool(spa_pool* pool);
 bool make_tensor_maps(spa_pool* pool, std::string* err);
 int device_sm_count(int* device_out);
+int current_device();   // cudaGetDevice, or -1
+spa_status check_device(const spa_pool* pool);   // pool.cpp: the calling thread's device is the pool's
 const char* cuda_error_string(int err);
 }  // namespace spa

@@ -33,9 +33,8 @@ def test_windowed_decode_after_release(family):
         vb = kv_bits_np(61, KIND_V, step, [0], np.arange(N), 4, 128)
         gb.pool.append(gb.reqs, [1] * N, bits_to_torch(kb), bits_to_torch(vb))
         rp.append_step(inp.batch, kb, vb)
-        # the query at the new token's position reads keys (n - W, n]: release before it
-        # with the window as seen from the PREVIOUS length, i.e. everything below n - W
-        gb.pool.release_window(gb.reqs, W + 1)
+        # the documented order: append, release the pages below n - W, plan with W
+        gb.pool.release_window(gb.reqs, W)
         plan.plan(gb.reqs, W)
         qb = families.kv_bits_np(5, 3, 70 + step, [0], np.arange(N), 16, 128)[0]
         o, lse = gb.decode(plan, 0, q_bits=qb)
@@ -64,7 +63,7 @@ def test_released_family_shares_and_matches_oracle(family):
                                           workloads.Group(333, 40, [17, 19])], seed=12)
     inp = families.make_inputs(rec, family)
     gb = GpuBatch(inp, num_pages=200)
-    gb.pool.release_window(list(gb.ids.values()), W + 1)
+    gb.pool.release_window(list(gb.ids.values()), W)
     rp = Replay(inp)
     for split in (0, 3):
         plan = spa.Plan(gb.pool, split_pages=split)

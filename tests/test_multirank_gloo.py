@@ -62,8 +62,8 @@ def _worker(rank, world, port, q):
         digests = [None] * world
         dist.all_gather_object(digests, _state_digest(pool, plan, reqs))
         # a windowed (local-layer) step after spa_kv_release_window replicates as well
-        pool.release_window(list(ids.values()), 1025)
         pool.append(reqs, [1] * len(reqs))
+        pool.release_window(list(ids.values()), 1024)
         plan.plan(reqs, 1024)
         wdig = [None] * world
         dist.all_gather_object(wdig, _state_digest(pool, plan, reqs))

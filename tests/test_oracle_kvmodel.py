@@ -169,8 +169,9 @@ def test_zero_and_full_prefix_forks():
 
 def test_release_window_rule_by_brute_force():
     """P7 pinned by its definition (reading #9): after release_window(W) at length n, every
-    key a future query (position q >= n, keys (q - W, q]) can read lies in a resident page,
-    and every released page holds only keys < n + 1 - W."""
+    key the current query (position n - 1, append-then-attend, reading #8) or a later one
+    (keys (q - W, q]) can read lies in a resident page, and every released page holds only
+    keys < n - W."""
     for n in range(0, 90, 7):
         for W in (1, 2, 15, 16, 17, 31, 32, 33, 64, 200):
             m = PagingModel(20, 16)
@@ -178,12 +179,12 @@ def test_release_window_rule_by_brute_force():
             assert m.append([r], [n]) == 0
             assert m.release_window([r], W) == 0
             t = m.tables[r]
-            for q in range(n, n + 40):                 # future queries (after more appends)
+            for q in range(max(0, n - 1), n + 40):      # the current query and later ones
                 for key in range(max(0, q + 1 - W), min(q + 1, n)):
                     assert t[key // 16] >= 0, (n, W, q, key)
             for i, p in enumerate(t):
                 if p < 0:
-                    assert (i + 1) * 16 <= n + 1 - W
+                    assert (i + 1) * 16 <= n - W
             m.check_invariants()
 
 
@@ -191,7 +192,7 @@ def test_release_window_hand_case_and_forks():
     m = PagingModel(20, 16)
     _, r = m.alloc()
     m.append([r], [100])                               # pages 0..6, keys 0..99
-    assert m.release_window([r], 32) == 0              # a query at 100 reads keys 69..100
+    assert m.release_window([r], 32) == 0              # the query at 99 reads keys 68..99
     assert m.tables[r] == [-1, -1, -1, -1, 4, 5, 6]    # pages 0-3 hold keys 0..63 only
     assert m.free_pages == list(range(0, 4)) + list(range(7, 20))
     st, c = m.fork(r, 96)                              # full pages only: -1 entries copied

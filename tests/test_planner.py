@@ -253,10 +253,10 @@ def test_window_release_bounds_a_local_layer_pool():
     reqs = [ids[n] for n in batch]
     used_full = pool.num_pages - len(pool.free_pages())
     W = 1024
-    pool.release_window(list(ids.values()), W + 1)
+    pool.release_window(list(ids.values()), W)
     for _ in range(40):
         pool.append(reqs, [1] * len(reqs))
-        pool.release_window(list(ids.values()), W + 1)
+        pool.release_window(list(ids.values()), W)
         plan = spa.Plan(pool)
         plan.plan(reqs, W)
     used = pool.num_pages - len(pool.free_pages())
@@ -277,7 +277,7 @@ def test_release_keeps_prefix_sharing_within_a_family():
     pool.append([parent], [5])
     reqs = [parent] + forks
     W = 200
-    pool.release_window(reqs, W + 1)
+    pool.release_window(reqs, W)
     assert len({pool.page_table(r)[1].count(-1) for r in reqs}) > 1     # different release points
     on, off = spa.Plan(pool), spa.Plan(pool, sharing=False)
     on.plan(reqs, W)
@@ -299,7 +299,26 @@ def test_release_family_grouping_with_parent_first_in_batch():
     pool.append(forks, [17, 19])
     pool.append([parent], [40])
     reqs = [parent] + forks
-    pool.release_window(reqs, 201)
+    pool.release_window(reqs, 200)
     plan = spa.Plan(pool)
     plan.plan(reqs, 200)
     assert plan.stats()["n_groups"] == 1
+
+
+def test_release_in_documented_order_never_breaks_the_plan():
+    """the documented per-step order -- append one token, release_window(W),
+    plan(W) -- must never leave the current query (at n - 1, append-then-attend, reading
+    #8) reaching a released page.  The old rule (16p + 16 <= n + 1 - W) failed every 16th
+    step; the oracle's P7 is the same rule (oracle/kvmodel.py)."""
+    W = 100
+    pool = spa.Pool(1, 8, 2, 128, 64)
+    r = pool.alloc()
+    pool.append([r], [1])
+    for n in range(2, 400):
+        pool.append([r], [1])
+        pool.release_window([r], W)
+        plan = spa.Plan(pool)
+        plan.plan([r], W)          # raises SpaError if the window needs a released page
+        t = pool.page_table(r)[1]
+        assert all(t[k // 16] >= 0 for k in range(max(0, n - W), n)), n
+        assert sum(p >= 0 for p in t) <= W // 16 + 2
