@@ -76,10 +76,15 @@ def launches(path):
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h, data = rows[hi], rows[hi + 1:]
     ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    mi = h.index("Metric Name")
+    ui = h.index("Metric Unit") if "Metric Unit" in h else None
+    to_ns = {"nsecond": 1.0, "ns": 1.0, "usecond": 1e3, "us": 1e3, "msecond": 1e6, "ms": 1e6}
     agg = collections.defaultdict(list)
     for r in data:
-        if len(r) > vi:
-            agg[r[ki].split("(")[0][:60]].append(float(r[vi].replace(",", "")))
+        # only the duration rows: a launch list taken with other metrics has bytes/cycles rows too
+        if len(r) > vi and r[mi] == "gpu__time_duration.sum":
+            scale = to_ns.get(r[ui], 1.0) if ui is not None else 1.0
+            agg[r[ki].split("(")[0][:60]].append(float(r[vi].replace(",", "")) * scale)
     tot = sum(sum(v) for v in agg.values())
     print(f"launch list {path}: {sum(len(v) for v in agg.values())} launches, {tot / 1e3:.1f} us total (ncu: serialised, cold)")
     for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
