@@ -286,6 +286,8 @@ def pages_for(recipe, extra_tokens):
     pages = 8
     for g in recipe.groups:
         pages += -(-(g.prefix + (g.parent_tail or 0) + extra_tokens) // 16)
+        if g.spec_prompt is not None:
+            pages += -(-(g.spec_prompt + 16 + extra_tokens) // 16)
         pages += sum(-(-(ft + 16 + extra_tokens) // 16) for ft in g.fork_tails)
     return pages
 

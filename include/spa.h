@@ -150,10 +150,14 @@ spa_status spa_pool_free_pages(const spa_pool* pool, int32_t* out_pages, int32_t
 
 /* ---------------------------------------------------------------------------------
  * Step plan (a4): built once per decode step on the host, uploaded once, reused by
- * every layer.  Groups are requests with the same first page; their shared region is
- * the longest common page-id prefix (reading #18).  Work items are
- * (KV head, group-split) and (KV head, member-tail-split); each shared page is read once
- * per (KV head, group) by one CTA-team holding all R = members x G query rows.
+ * every layer.  Groups are requests that hold a resident page in common (forks of one
+ * context, and forks of those).  Within a group, each maximal run of page indices over
+ * which the same set of requests holds the same pages is one range (a prefix tree:
+ * c_i shared by the main request and every speculative fork, a speculative prompt shared
+ * by the k samples forked from it, then private tails; reading #18).  Work items are
+ * (KV head, range split); each shared page is read once per (KV head, range) by one
+ * CTA-team holding all R = members x G query rows (ranges with more than max_rows rows
+ * are cut into chunks of max_rows rows that each read the pages).
  * --------------------------------------------------------------------------------- */
 typedef struct spa_plan_config {
     int32_t sharing;        /* 1: group by shared prefix (default); 0: every request alone (control) */
@@ -198,9 +202,12 @@ spa_status spa_extend_plan(spa_plan* plan, int32_t n_req, const spa_req* reqs, c
 
 typedef struct spa_plan_stats {
     int32_t n_req /* query rows */, n_groups, n_desc, n_items, n_records, n_teams, rows_max, generation;
-    int64_t unique_tokens;    /* sum over work descriptors of key tokens read, per KV head     */
-    int64_t unshared_tokens;  /* sum over requests of attended keys, per KV head (no sharing)  */
-    int64_t pages_read;       /* pages read per KV head (page-granular, incl. partial pages)   */
+    int64_t unique_tokens;    /* key tokens the work descriptors read, per KV head (a class cut
+                                 into max_rows chunks counts once per chunk)                     */
+    int64_t unshared_tokens;  /* sum over query rows of attended keys, per KV head (no sharing)  */
+    int64_t pages_read;       /* pages read per KV head (page-granular, incl. partial pages)     */
+    int64_t alg_tokens;       /* distinct (page, slot) keys any row attends to, per KV head: the
+                                 algorithmic lower bound of SURVEY.md Sec. 8(d) (B_alg / (Hkv d 4)) */
 } spa_plan_stats;
 spa_status spa_plan_get_stats(const spa_plan* plan, spa_plan_stats* out);
 

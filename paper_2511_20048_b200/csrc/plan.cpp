@@ -32,7 +32,7 @@ void plan_release(spa_plan* P);               // kernels.cu
 namespace {
 
 struct Range {
-    int kind;                 // 0 shared (group), 1 member tail
+    int kind;                 // bit 0: a row of the range also reads another range (partial records)
     int group;
     std::vector<int> members; // batch rows
     int32_t a, b;             // tokens [a, b)
@@ -149,6 +149,7 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
     const int Hkv = pool->cfg.num_kv_heads;
     const int G = pool->cfg.num_q_heads / Hkv;
     const int n_req = int(V.size());   // query rows
+    if (ps > 32) return fail(SPA_ERR_UNSUPPORTED, "plan: page_size > 32 (the planner keeps a 32-bit slot mask per page)");
     // window (reading #9): a query at position p attends to keys [p + 1 - W, p]
     std::vector<int32_t> lo(n_req);
     for (int i = 0; i < n_req; ++i) lo[i] = window > 0 ? std::max<int32_t>(0, V[i].hi - window) : 0;
@@ -211,79 +212,163 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
     }
     const int max_members = std::max(1, P->cfg.max_rows / G);
 
-    // ---- 2. ranges: the sub-group's common page-id prefix [., S) holds all its rows; each
-    //      request's rows share one tail range [., max hi) (per-row lo / hi are masks)
+    // ---- 2. ranges: a prefix tree of page-id runs per group (reading #18).  Sharing is
+    //      positional and prefix-shaped, so over page index k the requests of a group that
+    //      hold the same page at k form a class, and classes only split as k grows (between
+    //      the indices where some request's needed range starts or ends).  Each maximal run
+    //      of indices with the same class is one range holding the rows of exactly those
+    //      requests: c_i read once by the main request and all its speculative forks, the
+    //      speculative prompt read once by the k samples forked from it (PAPER.md:189, :198,
+    //      :335; nested forks, reading #17), each request's private tail by its own rows.
+    //      A class with more than max_rows / G rows is cut into chunks that re-read it.
     std::vector<Range> ranges;
     int n_groups = 0;
     int64_t unique_tokens = 0, unshared_tokens = 0;
     for (int i = 0; i < n_req; ++i) unshared_tokens += V[i].hi - lo[i];
+    // true algorithmic lower bound: distinct (page, slot) key positions any row attends to
+    int64_t alg_tokens = 0;
+    {
+        // page id -> bitmask of attended slots (ps <= 32), in a per-plan scratch array
+        auto& slots = P->slot_mask;
+        slots.resize(size_t(pool->cfg.num_pages), 0u);
+        std::vector<int32_t> touched;
+        for (int i = 0; i < n_req; ++i) {
+            const auto& t = V[i].req->pages;
+            const int32_t k0 = lo[i] / ps, k1 = int32_t(cdiv(V[i].hi, ps));
+            for (int32_t k = k0; k < k1; ++k) {
+                const int32_t pg = t[k];
+                if (pg < 0) continue;   // a released page: refused below
+                const int32_t a0 = k == k0 ? lo[i] - k * ps : 0;
+                const int32_t b0 = k == k1 - 1 ? V[i].hi - k * ps : ps;
+                const uint32_t bits = (b0 >= 32 ? 0xffffffffu : ((1u << b0) - 1u)) & ~((1u << a0) - 1u);
+                if (!slots[pg]) touched.push_back(pg);
+                slots[pg] |= bits;
+            }
+        }
+        for (int32_t pg : touched) {
+            alg_tokens += __builtin_popcount(slots[pg]);
+            slots[pg] = 0u;
+        }
+    }
+    struct Run {
+        std::vector<int> reqs;   // request indices (into U) of the class
+        int32_t k0, k1;          // page indices [k0, k1)
+    };
     for (const auto& grp : groups) {
-        for (size_t s0 = 0; s0 < grp.size(); s0 += max_members) {
-            std::vector<int> sg(grp.begin() + s0, grp.begin() + std::min(grp.size(), s0 + max_members));
-            const int gid = n_groups++;
-            // common page-id run [start, cp) of the sub-group: start = the first index every
-            // member holds (0 unless pages were released), S = cp * ps
-            int32_t cp = 0, start = 0;
-            bool one_table = true;
-            for (int m : sg) one_table &= V[m].req == V[sg[0]].req;
-            if (sg.size() > 1 && !one_table) {
-                for (int m : sg) start = std::max(start, d[m]);
-                const auto& t0 = V[sg[0]].req->pages;
-                for (cp = start;; ++cp) {
-                    bool ok = true;
-                    for (int m : sg) {
-                        const auto& t = V[m].req->pages;
-                        if (int64_t(V[m].hi) < int64_t(cp + 1) * ps || t[cp] != t0[cp]) { ok = false; break; }
-                    }
-                    if (!ok) break;
-                }
-                if (cp == start) cp = start = 0;   // nothing in common: every member reads its own range
+        const int gid = n_groups++;
+        // requests of the group (rows of one request are consecutive in V) and their needed
+        // token range [A, B) = [min lo, max hi) over their rows
+        std::vector<int> ufirst;            // first row of each request
+        std::vector<int> urow_end;          // one past its last row
+        for (size_t x = 0; x < grp.size();) {
+            size_t e = x;
+            while (e < grp.size() && V[grp[e]].req == V[grp[x]].req && grp[e] == grp[x] + int(e - x)) ++e;
+            ufirst.push_back(grp[x]);
+            urow_end.push_back(grp[e - 1] + 1);
+            x = e;
+        }
+        const int nu = int(ufirst.size());
+        std::vector<int32_t> A(nu), B(nu);
+        for (int u = 0; u < nu; ++u) {
+            A[u] = INT32_MAX;
+            B[u] = 0;
+            for (int r = ufirst[u]; r < urow_end[u]; ++r) {
+                A[u] = std::min(A[u], lo[r]);
+                B[u] = std::max(B[u], V[r].hi);
             }
-            const int32_t S = cp * ps, S0 = start * ps;
-            if (S > S0) {
-                std::vector<int> shared;
-                int32_t lo_min = S;
-                for (int m : sg)
-                    if (lo[m] < S) { shared.push_back(m); lo_min = std::min(lo_min, lo[m]); }
-                if (!shared.empty())
-                    ranges.push_back(Range{0, gid, shared, std::max(lo_min, S0), S, &V[sg[0]].req->pages});
-                // keys below the common run (a member that released fewer leading pages than
-                // another): read from the member's own table
-                for (size_t k = 0; k < sg.size();) {
-                    size_t e = k;
-                    while (e < sg.size() && V[sg[e]].req == V[sg[k]].req) ++e;
-                    std::vector<int> mem;
-                    int32_t a = INT32_MAX, b = 0;
-                    for (size_t x = k; x < e; ++x) {
-                        const int m = sg[x];
-                        if (lo[m] < S0) {
-                            mem.push_back(m);
-                            a = std::min(a, lo[m]);
-                            b = std::max(b, std::min(S0, V[m].hi));
-                        }
-                    }
-                    if (!mem.empty() && a < b) ranges.push_back(Range{1, gid, mem, a, b, &V[sg[k]].req->pages});
-                    k = e;
+        }
+        auto table = [&](int u) -> const std::vector<int32_t>& { return V[ufirst[u]].req->pages; };
+        // events: page indices where a request's needed range starts or ends
+        std::vector<int32_t> ev;
+        for (int u = 0; u < nu; ++u) {
+            ev.push_back(A[u] / ps);
+            ev.push_back(int32_t(cdiv(B[u], ps)));
+        }
+        std::sort(ev.begin(), ev.end());
+        ev.erase(std::unique(ev.begin(), ev.end()), ev.end());
+        std::vector<Run> runs;
+        // split S (all sharing page index k0, all active on [k0, k1)) into maximal runs
+        std::vector<std::pair<std::vector<int>, int32_t>> work;
+        for (size_t ei = 0; ei + 1 < ev.size(); ++ei) {
+            const int32_t k0 = ev[ei], k1 = ev[ei + 1];
+            std::vector<int> active;
+            for (int u = 0; u < nu; ++u)
+                if (A[u] / ps <= k0 && k0 < int32_t(cdiv(B[u], ps))) active.push_back(u);
+            if (active.empty()) continue;
+            auto partition = [&](const std::vector<int>& S, int32_t k) {
+                std::vector<std::pair<int32_t, std::vector<int>>> cls;   // (page id, members), first-seen order
+                for (int u : S) {
+                    const int32_t pg = table(u)[k];
+                    auto it = std::find_if(cls.begin(), cls.end(), [&](const auto& c) { return c.first == pg; });
+                    if (it == cls.end()) cls.push_back({pg, {u}});
+                    else it->second.push_back(u);
                 }
-            }
-            // per request (page table): its rows' keys beyond S
-            for (size_t k = 0; k < sg.size();) {
-                size_t e = k;
-                while (e < sg.size() && V[sg[e]].req == V[sg[k]].req) ++e;
-                std::vector<int> mem;
-                int32_t a = INT32_MAX, b = 0;
-                for (size_t x = k; x < e; ++x) {
-                    const int m = sg[x];
-                    const int32_t am = std::max(S, lo[m]);
-                    if (am < V[m].hi) {
-                        mem.push_back(m);
-                        a = std::min(a, am);
-                        b = std::max(b, V[m].hi);
+                for (auto& c : cls) work.push_back({std::move(c.second), k});
+            };
+            work.clear();
+            partition(active, k0);
+            while (!work.empty()) {
+                auto [S, ks] = std::move(work.back());
+                work.pop_back();
+                int32_t k = ks + 1;
+                if (S.size() > 1) {
+                    const auto& t0 = table(S[0]);
+                    for (; k < k1; ++k) {
+                        bool same = true;
+                        for (size_t x = 1; x < S.size() && same; ++x) same = table(S[x])[k] == t0[k];
+                        if (!same) break;
                     }
+                } else {
+                    k = k1;
                 }
-                if (!mem.empty()) ranges.push_back(Range{S > 0 ? 1 : 0, gid, mem, a, b, &V[sg[k]].req->pages});
-                k = e;
+                runs.push_back(Run{S, ks, k});
+                if (k < k1) partition(S, k);
             }
+        }
+        // merge runs of the same class that meet at an event boundary, then order by start
+        std::sort(runs.begin(), runs.end(), [](const Run& x, const Run& y) {
+            return x.reqs != y.reqs ? x.reqs < y.reqs : x.k0 < y.k0;
+        });
+        std::vector<Run> merged;
+        for (auto& r : runs) {
+            if (!merged.empty() && merged.back().reqs == r.reqs && merged.back().k1 == r.k0) merged.back().k1 = r.k1;
+            else merged.push_back(std::move(r));
+        }
+        std::stable_sort(merged.begin(), merged.end(), [](const Run& x, const Run& y) {
+            return x.reqs.size() != y.reqs.size() ? x.reqs.size() > y.reqs.size() : x.k0 < y.k0;
+        });
+        for (const auto& r : merged) {
+            int32_t a = INT32_MAX, b = 0;
+            for (int u : r.reqs) {
+                a = std::min(a, A[u]);
+                b = std::max(b, B[u]);
+            }
+            a = std::max(a, r.k0 * ps);
+            b = std::min(b, r.k1 * ps);
+            if (a >= b) continue;
+            // rows of the class whose own keys [lo, hi) meet [a, b), in batch order
+            std::vector<int> rows;
+            for (int u : r.reqs)
+                for (int x = ufirst[u]; x < urow_end[u]; ++x)
+                    if (lo[x] < b && V[x].hi > a) rows.push_back(x);
+            std::sort(rows.begin(), rows.end());
+            for (size_t c0 = 0; c0 < rows.size(); c0 += max_members) {
+                std::vector<int> chunk(rows.begin() + c0, rows.begin() + std::min(rows.size(), c0 + max_members));
+                // chunk rows may span requests: the page list is the same for all of them
+                ranges.push_back(Range{r.reqs.size() > 1 ? 0 : 1, gid, std::move(chunk), a, b, &table(r.reqs[0])});
+            }
+        }
+    }
+
+    // kind bit 0: some row of the range also takes part in another range (its outputs are
+    // partial records whatever the split) -- the split-size model below charges their cost
+    {
+        std::vector<int32_t> cnt(n_req, 0);
+        for (const auto& r : ranges)
+            for (int m : r.members) ++cnt[m];
+        for (auto& r : ranges) {
+            r.kind = 0;
+            for (int m : r.members) r.kind |= cnt[m] > 1 ? 1 : 0;
         }
     }
 
@@ -515,6 +600,7 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
     st.n_teams = T;
     st.rows_max = rows_max;
     st.unique_tokens = unique_tokens;
+    st.alg_tokens = alg_tokens;
     st.unshared_tokens = unshared_tokens;
     st.pages_read = pages_read;
     P->window = window;

@@ -112,6 +112,7 @@ struct spa_plan {
     int num_ctas = 0;
     // host view of the last plan
     std::vector<int32_t> host;  // header + arrays (also the upload source, pinned copy below)
+    std::vector<uint32_t> slot_mask;   // planner scratch: attended slots per page id (zero between plans)
     int32_t* pinned = nullptr;
     size_t pinned_words = 0;
     void* upload_event = nullptr;  // cudaEvent_t

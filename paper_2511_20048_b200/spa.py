@@ -46,7 +46,8 @@ class spa_plan_config(ctypes.Structure):
 class spa_plan_stats(ctypes.Structure):
     _fields_ = [("n_req", c_int32), ("n_groups", c_int32), ("n_desc", c_int32), ("n_items", c_int32),
                 ("n_records", c_int32), ("n_teams", c_int32), ("rows_max", c_int32), ("generation", c_int32),
-                ("unique_tokens", c_int64), ("unshared_tokens", c_int64), ("pages_read", c_int64)]
+                ("unique_tokens", c_int64), ("unshared_tokens", c_int64), ("pages_read", c_int64),
+                ("alg_tokens", c_int64)]
 
 
 # name -> (restype, argtypes); mirrors include/spa.h and include/spa_debug.h

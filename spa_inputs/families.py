@@ -13,6 +13,8 @@ mis-indexes pages.  These families make wrong gathers move O by O(1):
                needle_shared: needle inside the shared prefix c_i
                needle_tail:   one needle per member, inside the member's private tail
                needle_cow:    needle inside the copied partial page [16 floor(P/16), P)
+               needle_spec:   needle inside a nested speculative prompt (reading #17), for
+                              the samples forked from it (c_i for flat groups)
   *_pos      V is position-coded: v[j, g, c] = ((37 j + 11 c + 5 g + 3 o) mod 127 - 63)/32
              (o = origin stream id), so O ~ v[j*] identifies the gathered position.
 
@@ -29,11 +31,13 @@ import numpy as np
 from . import KIND_K, KIND_Q, KIND_V, MASK32, _combine, hash32, kv_bits_np
 from .workloads import Recipe, call_log
 
-FAMILIES = ("flat", "peaky", "needle_shared_pos", "needle_tail_pos", "needle_cow_pos", "flat_pos")
+FAMILIES = ("flat", "peaky", "needle_shared_pos", "needle_tail_pos", "needle_cow_pos", "needle_spec_pos", "flat_pos")
 
 
 def origin_id(name) -> int:
     gi, who = name
+    if who == "s":   # the nested speculative request (workloads.Group.spec_prompt)
+        return gi * 64 + 63
     return gi * 64 + (0 if who == "main" else 1 + int(who[1:]))
 
 
@@ -89,7 +93,7 @@ def make_inputs(recipe: Recipe, family: str = "flat", layers=None, step: int = 0
         q = _f32_to_bits(_bits_to_f32(q) * 4.0)
 
     needle_mode = None
-    for mode in ("needle_shared", "needle_tail", "needle_cow"):
+    for mode in ("needle_shared", "needle_tail", "needle_cow", "needle_spec"):
         if family.startswith(mode):
             needle_mode = mode
     pos_v = family.endswith("_pos")
@@ -101,16 +105,33 @@ def make_inputs(recipe: Recipe, family: str = "flat", layers=None, step: int = 0
     if needle_mode is not None:
         batch_idx = {nm: i for i, nm in enumerate(batch)}
         for gi, g in enumerate(recipe.groups):
+            # (name, tail start, tail length) of each batch member
+            sp = g.spec_prompt
+            at = g.prefix + (sp or 0)
             members = []
             if g.parent_tail is not None:
-                members.append(((gi, "main"), g.parent_tail))
-            members += [((gi, f"f{j}"), t) for j, t in enumerate(g.fork_tails)]
-            if needle_mode == "needle_shared" or (needle_mode == "needle_cow" and g.prefix % 16 == 0):
+                members.append(((gi, "main"), g.prefix, g.parent_tail))
+            if sp is not None and g.spec_in_batch:
+                members.append(((gi, "s"), g.prefix, sp))
+            members += [((gi, f"f{j}"), at, t) for j, t in enumerate(g.fork_tails)]
+            if needle_mode == "needle_spec":
+                # one needle in the speculative prompt, for the rows that read it: the samples
+                # (and the speculative request itself); groups without one fall back to c_i
+                if sp:
+                    base_key = ("spec", gi)
+                    pos = g.prefix + int(_small_ints(seed, 29 + gi, (1,), 0, sp - 1)[0])
+                    placements.setdefault(((gi, "s"), pos), []).append(base_key)
+                    needles[base_key] = pos
+                    for nm, _, _ in members:
+                        if nm[1] != "main":
+                            bases.setdefault(base_key, []).append(batch_idx[nm])
+                    continue
+            if needle_mode in ("needle_shared", "needle_spec") or (needle_mode == "needle_cow" and g.prefix % 16 == 0):
                 base_key = ("group", gi)
                 pos = int(_small_ints(seed, 11 + gi, (1,), 0, g.prefix - 1)[0])
                 placements.setdefault(((gi, "main"), pos), []).append(base_key)
                 needles[base_key] = pos
-                for nm, _ in members:
+                for nm, _, _ in members:
                     bases.setdefault(base_key, []).append(batch_idx[nm])
             elif needle_mode == "needle_cow":
                 base_key = ("group", gi)
@@ -118,14 +139,14 @@ def make_inputs(recipe: Recipe, family: str = "flat", layers=None, step: int = 0
                 pos = int(_small_ints(seed, 17 + gi, (1,), lo, g.prefix - 1)[0])
                 placements.setdefault(((gi, "main"), pos), []).append(base_key)
                 needles[base_key] = pos
-                for nm, _ in members:
+                for nm, _, _ in members:
                     bases.setdefault(base_key, []).append(batch_idx[nm])
             else:  # needle_tail
-                for nm, tail in members:
+                for nm, t0, tail in members:
                     if tail <= 0:
                         continue
                     base_key = ("member", nm)
-                    pos = g.prefix + int(_small_ints(seed, 23 + origin_id(nm), (1,), 0, tail - 1)[0])
+                    pos = t0 + int(_small_ints(seed, 23 + origin_id(nm), (1,), 0, tail - 1)[0])
                     placements.setdefault((nm, pos), []).append(base_key)
                     needles[base_key] = pos
                     bases.setdefault(base_key, []).append(batch_idx[nm])
@@ -144,7 +165,8 @@ def make_inputs(recipe: Recipe, family: str = "flat", layers=None, step: int = 0
 
     # needle amplitude 2^a from norms only (Cauchy-Schwarz): for every row
     #   scale * 2^a * (q_i . b) - scale * |q_i| * max_j |k_j| >= ln(n) + 8
-    n_max = max(g.prefix + max([g.parent_tail or 0] + list(g.fork_tails)) for g in recipe.groups)
+    n_max = max(g.prefix + (g.spec_prompt or 0) + max([g.parent_tail or 0] + list(g.fork_tails))
+                for g in recipe.groups)
     kmax = 3.9375 * np.sqrt(d)   # |k_j| <= max|entry| * sqrt(d) for counter-hash keys
     amp = {}
     for base_key, rows in bases.items():

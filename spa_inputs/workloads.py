@@ -46,6 +46,11 @@ class Group:
     prefix: int                 # |c_i|, tokens shared by every member
     parent_tail: int | None     # None: no main request in the batch (Aggressive phase)
     fork_tails: list[int] = field(default_factory=list)
+    # nested forks (reading #17): a speculative request "s" forks c_i and appends its
+    # speculation prompt of spec_prompt tokens (prefilled once); the k samples
+    # (fork_tails) then fork from s at prefix + spec_prompt instead of from main at prefix.
+    spec_prompt: int | None = None
+    spec_in_batch: bool = False   # s itself decodes in the batch (else it only holds the prompt)
 
 
 @dataclass
@@ -117,6 +122,22 @@ def sweep(batch: int, frac: float, seed: int | None = None) -> Recipe:
     return Recipe(f"sweep-B{batch}-f{frac}", QWEN25_32B, groups, seed=seed or 3000 + 10 * batch + fi)
 
 
+def nested(seed: int = 6, n_agents: int = 8, model: Model | None = None, prefix=(2048, 8192), k: int = 3) -> Recipe:
+    """Aggressive / Verified phase with nested forks (reading #17):
+    each agent's speculative request forks c_i and appends a 16-token speculation prompt, and
+    its k samples fork from it and decode U{1..10} tokens.  Agents alternate between the main
+    request present (Verified) and absent (Aggressive); every third agent's speculative
+    request also decodes."""
+    rng = np.random.default_rng(seed)
+    groups = []
+    for i in range(n_agents):
+        p = int(rng.integers(prefix[0], prefix[1] + 1))
+        t = int(rng.integers(0, 257)) if i % 2 == 0 else None
+        groups.append(Group(p, t, [int(rng.integers(1, 11)) for _ in range(k)], spec_prompt=16,
+                            spec_in_batch=i % 3 == 2))
+    return Recipe(f"nested-k{k}", model or QWEN25_32B, groups, seed=seed)
+
+
 def long32k(seed: int = 5, n_agents: int = 128) -> Recipe:
     """BJ config 4: 128 agents with 30k-32k contexts + 1 fork each."""
     rng = np.random.default_rng(seed)
@@ -128,9 +149,10 @@ def long32k(seed: int = 5, n_agents: int = 128) -> Recipe:
     return Recipe("long-32k", QWEN25_32B, groups, seed=seed)
 
 
-def random_small(seed: int, model: Model | None = None, max_prefix: int = 300) -> Recipe:
+def random_small(seed: int, model: Model | None = None, max_prefix: int = 300, nested: bool | None = None) -> Recipe:
     """Random small batches for parity tests: ragged prefixes (aligned and not), tails,
-    parent-less groups, nested shapes, multiple KV heads."""
+    parent-less groups, nested forks (samples of a speculative request, reading #17),
+    multiple KV heads.  nested: None = 30 % of seeds, True / False = force."""
     rng = np.random.default_rng(seed)
     if model is None:
         kv = int(rng.choice([1, 2, 4]))
@@ -144,6 +166,14 @@ def random_small(seed: int, model: Model | None = None, max_prefix: int = 300) -
         pt = int(rng.integers(0, 40)) if has_parent else None
         nf = int(rng.integers(0 if has_parent else 1, 4))
         groups.append(Group(p, pt, [int(rng.integers(0, 30)) for _ in range(nf)]))
+    # nested forks drawn after the flat groups, so earlier seeds keep their batches
+    if nested is None:
+        nested = rng.random() < 0.3
+    if nested:
+        for g in groups:
+            if g.fork_tails and rng.random() < 0.7:
+                g.spec_prompt = int(rng.integers(0, 40))
+                g.spec_in_batch = bool(rng.random() < 0.4)
     return Recipe(f"rand{seed}", model, groups, seed=seed)
 
 
@@ -156,7 +186,7 @@ def call_log(recipe: Recipe):
       ("append", name, origin, start, n)    -> append n tokens at logical positions
                                                [start, start+n) of stream `origin`
       ("fork", child, parent, prefix_len)
-    Names are ("g{i}", "main") / ("g{i}", "f{j}").  A parent-less group still allocates
+    Names are (i, "main") / (i, "s") (nested speculative request) / (i, "f{j}").  A parent-less group still allocates
     and fills its main request (the owner of c_i) but it is not part of the batch.
     `batch` lists the request names of the decode batch, group by group.
     """
@@ -166,14 +196,23 @@ def call_log(recipe: Recipe):
         main = (gi, "main")
         ops.append(("alloc", main))
         ops.append(("append", main, main, 0, g.prefix))
+        src, at = main, g.prefix
+        if g.spec_prompt is not None:   # nested: the samples fork from the speculative request
+            sp = (gi, "s")
+            ops.append(("fork", sp, main, g.prefix))
+            if g.spec_prompt:
+                ops.append(("append", sp, sp, g.prefix, g.spec_prompt))
+            src, at = sp, g.prefix + g.spec_prompt
         for j, ft in enumerate(g.fork_tails):
             ch = (gi, f"f{j}")
-            ops.append(("fork", ch, main, g.prefix))
+            ops.append(("fork", ch, src, at))
             if ft:
-                ops.append(("append", ch, ch, g.prefix, ft))
+                ops.append(("append", ch, ch, at, ft))
         if g.parent_tail:
             ops.append(("append", main, main, g.prefix, g.parent_tail))
         if g.parent_tail is not None:
             batch.append(main)
+        if g.spec_prompt is not None and g.spec_in_batch:
+            batch.append((gi, "s"))
         batch.extend((gi, f"f{j}") for j in range(len(g.fork_tails)))
     return ops, batch

@@ -28,6 +28,8 @@ def pages_needed(recipe, extra_tokens=0) -> int:
     n = 0
     for g in recipe.groups:
         n += -(-(g.prefix + (g.parent_tail or 0) + extra_tokens) // 16)
+        if g.spec_prompt is not None:   # the nested speculative request: CoW page + its prompt
+            n += -(-(g.spec_prompt + 16 + extra_tokens) // 16)
         n += sum(-(-(ft + 16 + extra_tokens) // 16) for ft in g.fork_tails)
     return n + 8
 
