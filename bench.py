@@ -292,14 +292,25 @@ def pages_for(recipe, extra_tokens):
     return pages
 
 
-def alg_bytes(st, N, hkv_l, hq_l, d, kv_elem=2):
-    """Algorithmic bytes of one decode_attention launch (per GPU): unique KV tokens per KV
-    head x Hkv_l x d x 2 (K, V) x kv_elem B (2 bf16, 1 fp8) + Q + O (bf16) + LSE (fp32) +
-    partials (fp32, w+r)."""
-    kv = st["unique_tokens"] * hkv_l * d * 2 * kv_elem
+def alg_bytes(st, N, hkv_l, hq_l, d, kv_elem=2, method=True):
+    """Algorithmic bytes of one decode_attention launch (per GPU), SURVEY.md Sec. 8(d) B_alg:
+    every distinct attended KV key read once (alg_tokens per KV head: distinct (page, slot)
+    positions) x Hkv_l x d x 2 (K, V) x kv_elem B (2 bf16, 1 fp8) + Q + O (bf16) + LSE
+    (fp32).  method=False adds the implementation's overheads (overhead_bytes)."""
+    kv = st["alg_tokens"] * hkv_l * d * 2 * kv_elem
     qo = N * hq_l * d * 2 * 2 + N * hq_l * 4
-    part = st["n_records"] * hq_l * (d + 1) * 4 * 2
-    return kv + qo + part
+    if method:
+        return kv + qo
+    o = overhead_bytes(st, hkv_l, hq_l, d, kv_elem)
+    return kv + qo + o["reread_kv"] + o["partials"]
+
+
+def overhead_bytes(st, hkv_l, hq_l, d, kv_elem=2):
+    """Bytes the plan moves beyond B_alg: KV keys read again by a class cut into max_rows
+    chunks (unique_tokens - alg_tokens; served by L2 when the chunks run close in time) and
+    the fp32 split partials (written, then read by the merge)."""
+    return {"reread_kv": (st["unique_tokens"] - st["alg_tokens"]) * hkv_l * d * 2 * kv_elem,
+            "partials": st["n_records"] * hq_l * (d + 1) * 4 * 2}
 
 
 # ----------------------------------------------------------------------------- main arm

@@ -71,16 +71,17 @@ constexpr int kQkChains = SPA_QK_CHAINS;   // independent HMMA accumulation chai
 
 constexpr int kSmemMax = 232448;   // 227 KB: the sm_100 per-block dynamic shared memory limit
 
-template <int D, int MT, int PPS, int TEAMS_, bool F8 = false>
+template <int D, int MT, int PPS, int TEAMS_, bool F8 = false, int KW_ = 2>
 struct DecodeCfg {
-    static constexpr int KW = 2;                          // key-split warps per row tile
+    static constexpr int KW = KW_;                        // key-split warps per row tile (1 or 2)
     static constexpr int TEAM_WARPS = MT * KW;
     static constexpr int TEAMS = TEAMS_;                  // teams (independent rings) per CTA
     static constexpr int WARPS = TEAMS * TEAM_WARPS;
     static constexpr int PAGE_BYTES = kPageSize * D * (F8 ? 1 : 2);  // K (or V) of one page, one head
     static constexpr int STAGE_BYTES = PPS * 2 * PAGE_BYTES;
     // per (team, row tile): column-half exchange [2][16][D/2] fp32 + (m, l) [2][16][2]
-    static constexpr int COMB_BYTES = TEAMS * MT * (2 * 16 * (D / 2) * 4 + 2 * 16 * 2 * 4);
+    // (KW = 1: a warp holds a row tile's whole state, nothing to exchange)
+    static constexpr int COMB_BYTES = KW == 2 ? TEAMS * MT * (2 * 16 * (D / 2) * 4 + 2 * 16 * 2 * 4) : 0;
     // barriers (full + empty), the team mailbox and the popped-item queue, for n stages
     static constexpr int misc(int n) { return TEAMS * n * 2 * 8 + TEAMS * 4 + TEAMS * (n + 2) * 32 + 16; }
     static constexpr int max_stages() {
@@ -99,15 +100,16 @@ struct DecodeCfg {
     static constexpr int SMEM = 1024 + OFF_COMB + COMB_BYTES;
     static_assert(NS >= 2 && (TEAMS < 4 || NS >= 3), "pipeline needs >= 2 stages (3 with 4 teams)");
     static_assert(PPS % KW == 0, "each key-split warp takes whole pages");
+    static_assert(KW == 1 || KW == 2, "one or two key-split warps per row tile");
     static_assert(OFF_COMB - OFF_BARS <= MISC_BYTES, "misc shared-memory region too small");
     static_assert(SMEM <= kSmemMax, "shared memory over the sm_100 limit");
 };
 
-template <int D, int MT, int PPS, int TEAMS, bool F8>
-__global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8>::WARPS * 32, 1)
+template <int D, int MT, int PPS, int TEAMS, bool F8, int KW_>
+__global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8, KW_>::WARPS * 32, 1)
     decode_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                   const __grid_constant__ DecodeParams p) {
-    using C = DecodeCfg<D, MT, PPS, TEAMS, F8>;
+    using C = DecodeCfg<D, MT, PPS, TEAMS, F8, KW_>;
     static_assert(!F8 || D == 128, "fp8 pages: d = 128");
     constexpr int KW = C::KW;
     constexpr int JW = PPS / KW;   // pages per warp per stage
@@ -564,9 +566,47 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8>::WARPS * 32, 
             }
         }
 
-        // ---- epilogue: combine the KW key-split states of each row tile, normalise, and
-        //      write each column half (warp wk owns columns [wk D/2, (wk+1) D/2)).
-        if (active) {
+        // ---- epilogue (KW = 1): the warp holds its row tile's whole state; normalise and
+        //      write every column
+        if constexpr (KW == 1) {
+            if (active) {
+                l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+                l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+                l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+                l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+                const int c0 = 2 * (lane & 3);
+#pragma unroll
+                for (int rr = 0; rr < 2; ++rr) {
+                    const int row = rr ? row1 : row0;
+                    if (row < R) {
+                        const int mb = row / G;
+                        const Member m = mems[dsc.member_off + mb];
+                        const int head = itm.kv_head * G + (row - mb * G);
+                        const float l = rr ? l1 : l0;
+                        const float mm = rr ? m1 : m0;
+                        const float inv = l > 0.f ? v_scale / l : 0.f;
+                        const float lse = l > 0.f ? (mm + log2f(l)) * 0.69314718055994531f : -INFINITY;
+                        if (m.rec < 0) {
+                            __nv_bfloat16* orow = p.o + m.row * p.o_sr + head * p.o_sh;
+#pragma unroll
+                            for (int n = 0; n < NT; ++n)
+                                st_out2(fan, orow + n * 8 + c0, acc[n][2 * rr] * inv, acc[n][2 * rr + 1] * inv);
+                            if ((lane & 3) == 0 && p.lse) st_out1(fan, p.lse + m.row * p.l_sr + head * p.l_sh, lse);
+                        } else {
+                            float* prow = p.part_o + ((long long)m.rec * Hq + head) * D;
+#pragma unroll
+                            for (int n = 0; n < NT; ++n)
+                                *reinterpret_cast<float2*>(prow + n * 8 + c0) =
+                                    make_float2(acc[n][2 * rr] * inv, acc[n][2 * rr + 1] * inv);
+                            if ((lane & 3) == 0) p.part_lse[(long long)m.rec * Hq + head] = lse;
+                        }
+                    }
+                }
+            }
+        }
+        // ---- epilogue (KW = 2): combine the two key-split states of each row tile,
+        //      normalise, and write each column half (warp wk owns columns [wk D/2, (wk+1) D/2)).
+        if (KW == 2 && active) {
             l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
             l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
             l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
@@ -761,15 +801,15 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8>::WARPS * 32, 
     }
 }
 
-template <int D, int MT, int PPS, int TEAMS, bool F8 = false>
+template <int D, int MT, int PPS, int TEAMS, bool F8 = false, int KW = 2>
 static int launch_decode_t(const spa_plan* P, const DecodeParams& dp, void* stream) {
-    using C = DecodeCfg<D, MT, PPS, TEAMS, F8>;
+    using C = DecodeCfg<D, MT, PPS, TEAMS, F8, KW>;
     static std::atomic<unsigned long long> attr_done{0};
-    if (int e = set_smem_attr_once(decode_kernel<D, MT, PPS, TEAMS, F8>, C::SMEM, &attr_done)) return e;
+    if (int e = set_smem_attr_once(decode_kernel<D, MT, PPS, TEAMS, F8, KW>, C::SMEM, &attr_done)) return e;
     const CUtensorMap* tk = reinterpret_cast<const CUtensorMap*>(P->pool->tmap_k.bytes);
     const CUtensorMap* tv = reinterpret_cast<const CUtensorMap*>(P->pool->tmap_v.bytes);
-    return launch_pdl(decode_kernel<D, MT, PPS, TEAMS, F8>, dim3(P->num_ctas), dim3(C::WARPS * 32), C::SMEM, stream,
-                      *tk, *tv, dp);
+    return launch_pdl(decode_kernel<D, MT, PPS, TEAMS, F8, KW>, dim3(P->num_ctas), dim3(C::WARPS * 32), C::SMEM,
+                      stream, *tk, *tv, dp);
 }
 
 // F4 fp8 pages (d = 128): the same team shapes as bf16; SPA_F8_PPS pages per stage (4: the
@@ -791,6 +831,8 @@ static int launch_decode_f8(const spa_plan* P, const DecodeParams& dp, void* str
 
 template <int D>
 static int launch_decode_d(const spa_plan* P, const DecodeParams& dp, void* stream) {
+    // 32-row items, one warp per row tile over every page of a stage (no key split): 4 teams
+    if (P->mt == 2 && P->kw == 1) return launch_decode_t<D, 2, 2, 4, false, 1>(P, dp, stream);
     if (P->mt == 1) {
         if (P->teams == 1) return launch_decode_t<D, 1, 2, 1>(P, dp, stream);
         if (P->teams == 2) return launch_decode_t<D, 1, 2, 2>(P, dp, stream);
@@ -801,7 +843,8 @@ static int launch_decode_d(const spa_plan* P, const DecodeParams& dp, void* stre
     return launch_decode_t<D, 2, 2, 2>(P, dp, stream);
 }
 
-bool decode_teams_supported(int mt, int teams) {
+bool decode_teams_supported(int mt, int teams, int kw) {
+    if (kw == 1) return mt == 2 && teams == 4;
     if (mt == 4 || mt == 8) return teams == 1;
     return teams == 1 || teams == 2 || (teams == 4 && mt == 1);
 }
@@ -811,6 +854,7 @@ int launch_decode(const spa_plan* P, int32_t layer, const void* q, int64_t q_sr,
                   const PeerLaunch* peer) {
     if (peer && (P->mt == 8 || P->cfg.merge_mode == 2)) return int(cudaErrorNotSupported);
     if (P->pool->kv_fp8 && P->mt == 8) return int(cudaErrorNotSupported);   // the tcgen05 extend kernel is bf16
+    if (P->pool->kv_fp8 && P->kw == 1) return int(cudaErrorNotSupported);   // fp8: two key-split warps only
     if (P->mt == 8)   // 128-row items: the tcgen05 extend kernel (ext.cu)
         return launch_ext(P, layer, q, q_sr, q_sh, o, o_sr, o_sh, lse, l_sr, l_sh, scale, stream);
     const auto& c = P->pool->cfg;

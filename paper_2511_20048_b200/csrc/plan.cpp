@@ -72,14 +72,18 @@ spa_status spa_plan_create(spa_pool* pool, const spa_plan_config* cfg, spa_plan*
     P->num_ctas = ctas;
     int teams = c.teams_per_cta;
     if (const char* e = std::getenv("SPA_TEAMS")) teams = std::atoi(e);
-    if (teams == 0) teams = P->mt == 1 ? 4 : P->mt == 2 ? 2 : 1;
+    // 32-row items: SPA_KW=1 selects one warp per row tile over every page of a stage
+    int kw = 2;
+    if (const char* e = std::getenv("SPA_KW")) kw = std::atoi(e) == 1 && P->mt == 2 ? 1 : 2;
+    if (teams == 0) teams = kw == 1 ? 4 : P->mt == 1 ? 4 : P->mt == 2 ? 2 : 1;
     if (P->mt == 8 && c.merge_mode != 2 && c.merge_mode != 0)
         return fail(SPA_ERR_UNSUPPORTED, "max_rows 128 merges split partials with the merge kernel");
-    if (!decode_teams_supported(P->mt, teams)) {
+    if (!decode_teams_supported(P->mt, teams, kw)) {
         delete P;
         return fail(SPA_ERR_UNSUPPORTED, "teams_per_cta must be 1, 2 or 4 (4 only with max_rows 16, 1 with 64)");
     }
     P->teams = teams;
+    P->kw = kw;
     P->n_teams = ctas * teams;
     *out = P;
     return SPA_OK;
@@ -544,7 +548,7 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
         // parallel, ~one L2 round trip after its last record; G <= max_rows <= 128 < 255) or,
         // when there are many more head merges than warps, task * 256 + 0 (one warp merges all G heads of the task with
         // their loads in flight together: fewer, longer subtasks; needs G x S <= 32)
-        const int64_t warps_total = int64_t(P->num_ctas) * P->teams * P->mt * 2;
+        const int64_t warps_total = int64_t(P->num_ctas) * P->teams * P->mt * P->kw;
         bool whole = int64_t(tasks.size()) * G > 4 * warps_total;
         if (const char* e = std::getenv("SPA_MERGE_WHOLE")) whole = std::atoi(e) != 0;   // tests: force a path
         for (int32_t t : tasks) {
@@ -660,7 +664,7 @@ spa_status spa_debug_plan_geometry(const spa_plan* plan, int32_t* out_num_ctas, 
         return fail(SPA_ERR_INVALID_ARG, "null argument");
     *out_num_ctas = plan->num_ctas;
     *out_teams_per_cta = plan->teams;
-    *out_warps_per_cta = plan->teams * plan->mt * 2;   // a team = mt row tiles x 2 key-split warps
+    *out_warps_per_cta = plan->teams * plan->mt * plan->kw;   // a team = mt row tiles x kw key-split warps
     return SPA_OK;
 }
 

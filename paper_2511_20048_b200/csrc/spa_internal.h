@@ -108,6 +108,7 @@ struct spa_plan {
     spa_plan_config cfg{};
     int mt = 1;                 // m16 tiles (warps) per team: max_rows / 16
     int teams = 4;              // teams (work-item streams with private rings) per CTA
+    int kw = 2;                 // key-split warps per row tile (1: a warp takes every page of a stage)
     int n_teams = 0;
     int num_ctas = 0;
     // host view of the last plan
@@ -179,7 +180,7 @@ int launch_decode(const spa_plan* plan, int32_t layer, const void* q, int64_t q_
 int launch_merge(int32_t n_req, int32_t num_heads, int32_t head_dim, const int32_t* rec_ptr, const float* part_o,
                  const float* part_lse, void* o, int64_t o_sr, int64_t o_sh, float* lse, int64_t l_sr, int64_t l_sh,
                  int grid_hint, void* stream);
-bool decode_teams_supported(int mt, int teams);   // decode.cu: compiled (row tiles, teams/CTA)
+bool decode_teams_supported(int mt, int teams, int kw);   // decode.cu: compiled (row tiles, teams/CTA, key split)
 // ext.cu: the tcgen05 kernel for 128-row (extend) plans
 bool ext_supported(int head_dim);
 int launch_ext(const spa_plan* plan, int32_t layer, const void* q, int64_t q_sr, int64_t q_sh, void* o, int64_t o_sr,

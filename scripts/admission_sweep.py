@@ -76,7 +76,7 @@ def main():
             torch.cuda.synchronize()
             layer_us = e0.elapsed_time(e1) * 1e3 / (reps * Lr)
             st = plan.stats()
-            kv = st["unique_tokens"] * m.num_kv_heads * m.head_dim * 4
+            kv = st["alg_tokens"] * m.num_kv_heads * m.head_dim * 4
             row = {"cap": cap, "policy": policy, "admitted": N,
                    "speculative": sum(1 for nm in names if nm[1] != "main"),
                    "main": sum(1 for nm in names if nm[1] == "main"),

@@ -59,12 +59,10 @@ def main():
     plan = spa.Plan(pool, max_rows=a.max_rows)
     plan.plan(reqs, 0, stream=stream, n_query=nq)
     st = plan.stats()
-    dplan = spa.Plan(pool)                      # the decode plan of the same requests:
-    dplan.plan(reqs, 0, stream=stream)          # its unique keys = the sharing lower bound
-    kv_alg_tokens = dplan.stats()["unique_tokens"]
+    kv_alg_tokens = st["alg_tokens"]            # distinct attended keys: the sharing lower bound
     d = m.head_dim
     alg = kv_alg_tokens * m.num_kv_heads * d * 2 * 2 + rows * m.num_q_heads * (d * 2 * 2 + 4)
-    plan_bytes = bench.alg_bytes(st, rows, m.num_kv_heads, m.num_q_heads, d)
+    plan_bytes = bench.alg_bytes(st, rows, m.num_kv_heads, m.num_q_heads, d, method=False)
     # flops: QK^T and PV over every row's live keys
     keys = 0
     for n, t in zip(lens, nq):

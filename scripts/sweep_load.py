@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--resident", type=int, default=8)
     ap.add_argument("--calls", type=int, default=64)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--plans", default="", help="comma list of plan keys to run (default: all)")
     a = ap.parse_args()
     batches = [int(x) for x in a.batches.split(",")]
     fracs = [float(x) for x in a.fracs.split(",")]
@@ -46,7 +47,13 @@ def main():
     # one pool for every point: sized for the largest batch
     pages = max(bench.pages_for(workloads.sweep(b, f), 8) for b in batches for f in fracs)
     pool = spa.Pool(Lr, m.num_q_heads, m.num_kv_heads, m.head_dim, pages, device=dev)
-    plans = {"shared": spa.Plan(pool), "shared32": spa.Plan(pool, max_rows=32), "unshared": spa.Plan(pool, sharing=False)}
+    plans = {"shared": spa.Plan(pool), "shared32": spa.Plan(pool, max_rows=32)}
+    os.environ["SPA_KW"] = "1"          # 32-row items, one warp per row tile, no key split
+    plans["shared32kw1"] = spa.Plan(pool, max_rows=32)
+    del os.environ["SPA_KW"]
+    plans["unshared"] = spa.Plan(pool, sharing=False)
+    if a.plans:
+        plans = {k: v for k, v in plans.items() if k in a.plans.split(",")}
     rows = []
     out = open(a.out, "w")
     for b in batches:
@@ -78,19 +85,19 @@ def main():
                     torch.cuda.synchronize()
                     ts.append(e0.elapsed_time(e1) / a.calls)
                 layer_ms = float(np.median(ts))
-                ab = bench.alg_bytes(st, N, m.num_kv_heads, m.num_q_heads, m.head_dim)
+                ab = bench.alg_bytes(st, N, m.num_kv_heads, m.num_q_heads, m.head_dim)   # method bytes (B_alg)
                 rec_row[key] = {"layer_us": layer_ms * 1e3, "attn_ms_per_step": layer_ms * m.num_layers,
                                 "tokens_per_s": N / (layer_ms * 1e-3 * m.num_layers),
-                                "alg_gbs": ab / (layer_ms * 1e-3) / 1e9, "kv_tokens_per_head": st["unique_tokens"],
+                                "alg_gbs": ab / (layer_ms * 1e-3) / 1e9, "alg_tokens_per_head": st["alg_tokens"],
+                                "read_tokens_per_head": st["unique_tokens"],
+                                "overhead_bytes": bench.overhead_bytes(st, m.num_kv_heads, m.num_q_heads, m.head_dim),
                                 "records": st["n_records"]}
             rows.append(rec_row)
             out.write(json.dumps(rec_row) + "\n")
             out.flush()
-            sh, s32, us = rec_row["shared"], rec_row["shared32"], rec_row["unshared"]
-            print(f"B={b:4d} f={f:4.2f} N={N:4d}  shared {sh['layer_us']:7.1f} us {sh['tokens_per_s']:7.0f} tok/s "
-                  f"{sh['alg_gbs']:5.0f} GB/s | rows32 {s32['layer_us']:7.1f} us | unshared {us['layer_us']:7.1f} us "
-                  f"{us['tokens_per_s']:7.0f} tok/s | sharing speedup {us['layer_us'] / min(sh['layer_us'], s32['layer_us']):.2f}x",
-                  flush=True)
+            print(f"B={b:4d} f={f:4.2f} N={N:4d} " + " | ".join(
+                f"{k} {v['layer_us']:7.1f} us {v['tokens_per_s']:7.0f} tok/s {v['alg_gbs']:5.0f} GB/s"
+                for k, v in rec_row.items() if isinstance(v, dict)), flush=True)
             for nm in ids.values():   # release the batch (and the parents of forks)
                 pool.free(nm)
     out.close()

@@ -135,6 +135,7 @@ def main():
     ap.add_argument("--merge", type=int, default=0)
     ap.add_argument("--out", default=None)
     ap.add_argument("--kv", default="bf16", choices=["bf16", "fp8"])
+    ap.add_argument("--rows", type=int, default=16, help="plan max_rows (16, 32, 64)")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     stream = torch.cuda.Stream()
@@ -156,7 +157,7 @@ def main():
     q = kv_bits_torch(rec.seed, KIND_Q, 1, list(range(Lr)), np.arange(N), m.num_q_heads, m.head_dim, dev).contiguous()
     o = torch.empty((Lr, N, m.num_q_heads, m.head_dim), dtype=torch.bfloat16, device=dev)
     lse = torch.empty((Lr, N, m.num_q_heads), dtype=torch.float32, device=dev)
-    plan = spa.Plan(pool, split_pages=a.split, merge_mode=a.merge, teams_per_cta=a.teams)
+    plan = spa.Plan(pool, split_pages=a.split, merge_mode=a.merge, teams_per_cta=a.teams, max_rows=a.rows)
     plan.plan(reqs, 0, stream=stream)
     st = plan.stats()
 
@@ -197,7 +198,7 @@ def main():
     buf = plan.set_trace(256)   # zeroed on the stream; the traced launch follows 7 chained ones
     plan.decode(7 % Lr, q[7 % Lr], o[7 % Lr], lse[7 % Lr], scale=m.softmax_scale, stream=stream)
     torch.cuda.synchronize()
-    res = {"workload": a.workload, "N": N, "stats": st, "eager_chained_us": eager_us,
+    res = {"workload": a.workload, "rows": a.rows, "N": N, "stats": st, "eager_chained_us": eager_us,
            "graph_chained_us": float(np.median(graph_us)), "host_us_per_call": host_us,
            "alg_bytes": bench.alg_bytes(st, N, m.num_kv_heads, m.num_q_heads, m.head_dim, 1 if fp8 else 2), "kv": a.kv}
     res["trace"] = analyse(buf)
@@ -206,6 +207,7 @@ def main():
     item_pages = [descs[d][1] for d, _ in items]
     res["rates"] = team_rates(buf, item_pages, buf.shape[0] // plan.num_ctas_hint())
     res["graph_gbs"] = res["alg_bytes"] / (res["graph_chained_us"] * 1e-6) / 1e9
+    res["overhead_bytes"] = bench.overhead_bytes(st, m.num_kv_heads, m.num_q_heads, m.head_dim, 1 if fp8 else 2)
     plan.set_trace(0)
     print(json.dumps(res), flush=True)
     if a.out:

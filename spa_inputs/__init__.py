@@ -94,6 +94,56 @@ def q_bits_np(seed: int, step: int, layers, n_req: int, n_heads: int, head_dim: 
     return kv_bits_np(seed, KIND_Q, step, layers, np.arange(n_req), n_heads, head_dim)
 
 
+# ----------------------------------------------------------------------------- full-precision values
+# The counter-hash values above sit on a 7-bit grid (multiples of 1/32, |32 v| <= 126), so
+# they never set the bf16 mantissa LSB and keep every q.k product exact in fp32.  These
+# generators fill the whole bf16 format (parity inputs too narrow):
+#
+#   normal(sigma)   v = RNE_bf16(fp32(sigma * z)), z ~ N(0, 1) by Box-Muller from two
+#                   counter hashes (float64 NumPy; host only);
+#   wide(emin, emax) random sign, exponent uniform in [emin, emax], all 7 mantissa bits from
+#                   the hash: integer ops only, bit-identical in NumPy and torch.
+
+
+def _bf16_rne_bits(f32):
+    """bf16 bits of float32 values, round to nearest even (finite inputs)."""
+    u = np.asarray(f32, np.float32).view(np.uint32).astype(np.int64)
+    return (((u + 0x7FFF + ((u >> 16) & 1)) >> 16) & 0xFFFF).astype(np.uint16)
+
+
+def _hash_grid_np(seed, kind, origin, layers, positions, n_heads, head_dim, salt=0):
+    kl = stream_key_np(seed, kind, origin, layers, positions)
+    hc = channel_key_np(n_heads, head_dim)
+    if salt:
+        hc = _combine(hc, np.int64(salt))
+    L, T = kl.shape
+    return _combine(kl[:, :, None], hc[None, None, :]).reshape(L, T, n_heads, head_dim)
+
+
+def normal_bits_np(sigma: float, seed, kind, origin, layers, positions, n_heads, head_dim):
+    """bf16 bits [L, T, H, d] of RNE_bf16(fp32(sigma * z)), z ~ N(0, 1) (Box-Muller)."""
+    h1 = _hash_grid_np(seed, kind, origin, layers, positions, n_heads, head_dim)
+    h2 = hash32((h1 ^ 0x9E3779B9) & MASK32)
+    u1 = (h1.astype(np.float64) + 0.5) / 4294967296.0
+    u2 = h2.astype(np.float64) / 4294967296.0
+    z = np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * np.pi * u2)
+    return _bf16_rne_bits((sigma * z).astype(np.float32))
+
+
+def _wide_from_hash(h, emin: int, emax: int):
+    sign = (h >> 31) & 1
+    e = emin + (h & 0xFFFF) % (emax - emin + 1)
+    mant = (h >> 16) & 0x7F
+    return (sign << 15) | ((e + 127) << 7) | mant
+
+
+def wide_bits_np(emin: int, emax: int, seed, kind, origin, layers, positions, n_heads, head_dim):
+    """bf16 bits [L, T, H, d]: random sign, exponent uniform in [emin, emax] (|v| in
+    [2^emin, 2^(emax+1))), random 7-bit mantissa."""
+    h = _hash_grid_np(seed, kind, origin, layers, positions, n_heads, head_dim, salt=0x5bd1e995)
+    return _wide_from_hash(h, emin, emax).astype(np.uint16)
+
+
 # ----------------------------------------------------------------------------- torch
 def _torch():
     import torch  # noqa: WPS433 (lazy: the oracle side never needs torch)
@@ -115,6 +165,18 @@ def kv_bits_torch(seed: int, kind: int, origin: int, layers, positions, n_heads:
     v = (s.to(torch.float32) / 32.0).to(torch.bfloat16)
     L, T = kl.shape
     return v.reshape(L, T, n_heads, head_dim)
+
+
+def wide_bits_torch(emin: int, emax: int, seed, kind, origin, layers, positions, n_heads, head_dim, device="cuda"):
+    """wide_bits_np on `device` with torch int64 ops (bit-identical); returns torch.bfloat16."""
+    torch = _torch()
+    kl = torch.from_numpy(stream_key_np(seed, kind, origin, layers, positions)).to(device)
+    hc = torch.from_numpy(_combine(channel_key_np(n_heads, head_dim), np.int64(0x5bd1e995))).to(device)
+    h = hash32((kl[:, :, None] ^ hc[None, None, :]) & MASK32)
+    b = _wide_from_hash(h, emin, emax)
+    b = torch.where(b >= 32768, b - 65536, b).to(torch.int16)
+    L, T = kl.shape
+    return b.view(torch.bfloat16).reshape(L, T, n_heads, head_dim)
 
 
 def bits_to_f64(bits) -> np.ndarray:

@@ -115,3 +115,43 @@ def run_parity(recipe, family="flat", window=0, sharing=True, max_rows=16, split
         errs.append(compare(o, lse, O_ref, L_ref))
         outs.append((o, lse))
     return errs, outs, gb, plan, rp
+
+
+def derived_tolerance(rp: Replay, layer_pos: int, q_bits: np.ndarray, window: int = 0, names=None, scale=None):
+    """Per (row, head) error bounds of the bf16 decode path ("Error budget"),
+    from the inputs only:
+
+        tol_O   = V* (2^-8 + 2^-16 (1 + Z1)) + 2^-24
+        tol_LSE = 2^-18 (1 + Z1) + 2^-21 |LSE| + n 2^-24 + 2^-20
+
+    V* = max |v| over the attended keys, Z1 = scale max_j sum_c |q_c k_jc|, n = keys.
+    2^-9 (P rounded to bf16 for PV) + 2^-9 (O rounded to bf16) give the 2^-8; the fp32
+    accumulation of q.k over d = 128 (8 k16 MMA steps, <= 2^-19 sum |q k| worst case) gives
+    a logit error <= 2^-18 Z1 and a relative weight error <= 2 of that."""
+    m = rp.inputs.recipe.model
+    scale = m.softmax_scale if scale is None else scale
+    names = rp.inputs.batch if names is None else names
+    G = m.num_q_heads // m.num_kv_heads
+    tol_o = np.zeros((len(names), m.num_q_heads))
+    tol_l = np.zeros((len(names), m.num_q_heads))
+    O_ref, L_ref = rp.expected(layer_pos, q_bits, names=names, window=window, scale=scale)
+    for i, nm in enumerate(names):
+        K, V = rp.kv_f64(nm, layer_pos)
+        n = K.shape[0]
+        lo = max(0, n - window) if window > 0 else 0
+        K, V = K[lo:], V[lo:]
+        q = (np.asarray(q_bits[i]).astype(np.uint16).astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+        for h in range(m.num_q_heads):
+            g = h // G
+            vstar = np.abs(V[:, g]).max()
+            z1 = scale * (np.abs(K[:, g]) @ np.abs(q[h])).max()
+            tol_o[i, h] = vstar * (2.0 ** -8 + 2.0 ** -16 * (1 + z1)) + 2.0 ** -24
+            tol_l[i, h] = 2.0 ** -18 * (1 + z1) + 2.0 ** -21 * abs(L_ref[i, h]) + K.shape[0] * 2.0 ** -24 + 2.0 ** -20
+    return O_ref, L_ref, tol_o, tol_l
+
+
+def compare_rows(o: torch.Tensor, lse: torch.Tensor, O_ref: np.ndarray, L_ref: np.ndarray):
+    """(|O - O_ref| max over channels [N, Hq], |LSE - LSE_ref| [N, Hq])."""
+    og = o.float().cpu().numpy().astype(np.float64)
+    lg = lse.cpu().numpy().astype(np.float64)
+    return np.abs(og - O_ref).max(axis=-1), np.abs(lg - L_ref)

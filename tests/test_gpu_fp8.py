@@ -132,3 +132,30 @@ def test_fp8_rejections():
     with pytest.raises(spa.SpaError) as e:
         gb.decode(plan, 0)
     assert e.value.status == spa.SPA_ERR_CUDA
+
+
+@pytest.mark.parametrize("family", ["flat", "needle_shared_pos", "full_n1"])
+def test_fp8_error_against_the_bf16_oracle(family):
+    """FP8 pages change the inputs: report the error against the oracle on the bf16 K/V
+     and bound it by the quantisation error itself plus the parity gate:
+    |O_gpu - O_bf16| <= |O_deq - O_bf16| + 2e-2 elementwise, O_deq = the oracle on the
+    dequantised K/V (oracle/fp8.py), likewise for the LSE with 1e-3."""
+    rec = workloads.qwen(seed=3, n_agents=4)
+    for g in rec.groups:
+        g.prefix = 300 + g.prefix % 500
+    rec.model = _model(1)
+    inp = families.make_inputs(rec, family)
+    sc = fp8_scales(inp)
+    gb = GpuBatch(inp, kv_scale=sc)
+    plan = spa.Plan(gb.pool, split_pages=4)
+    plan.plan(gb.reqs)
+    o, lse = gb.decode(plan, 0)
+    O_bf, L_bf = Replay(inp).expected(0, inp.q[0])
+    O_dq, L_dq = Replay(inp, kv_fp8_scale=sc).expected(0, inp.q[0])
+    og = o.float().cpu().numpy().astype(np.float64)
+    lg = lse.cpu().numpy().astype(np.float64)
+    e_gpu, e_q = np.abs(og - O_bf), np.abs(O_dq - O_bf)
+    assert (e_gpu <= e_q + O_TOL).all()
+    assert (np.abs(lg - L_bf) <= np.abs(L_dq - L_bf) + LSE_TOL).all()
+    print(f"\nfp8 vs bf16 oracle [{family}]: max|dO| {e_gpu.max():.4f} (quantisation alone {e_q.max():.4f}), "
+          f"rms {np.sqrt((e_gpu ** 2).mean()):.5f}, max|dLSE| {np.abs(lg - L_bf).max():.4f}")
