@@ -161,8 +161,12 @@ spa_status spa_pool_free_pages(const spa_pool* pool, int32_t* out_pages, int32_t
  * --------------------------------------------------------------------------------- */
 typedef struct spa_plan_config {
     int32_t sharing;        /* 1: group by shared prefix (default); 0: every request alone (control) */
-    int32_t max_rows;       /* 16, 32 or 64: query rows (rows x G) per work item; larger groups
-                               are cut into sub-groups.  0 = 16 (64: extend batches, one team)  */
+    int32_t max_rows;       /* 16, 32, 64 or 128: query rows (requests x G) per work item; a range
+                               with more rows is cut into chunks that each read its pages.
+                               0 (default) = auto: per batch, 32 when ranges of more than 16
+                               rows (k = 3 forks of a G = 5 context: 20 rows) hold > 30 % of the
+                               pages, else 16 (G > 16: 32).  64: extend batches, one team;
+                               128: the tcgen05 extend kernel (bf16, head_dim 128)              */
     int32_t split_pages;    /* max pages per split; 0 = auto (balance over the persistent grid)  */
     int32_t num_ctas;       /* persistent grid size; 0 = number of SMs                            */
     int32_t merge_mode;     /* where split partials are merged (spa_merge_splits semantics always):
@@ -173,7 +177,10 @@ typedef struct spa_plan_config {
                                2: by a separate merge_kernel launch (programmatic dependent launch) */
     int32_t teams_per_cta;  /* work-item streams per CTA, each with a private shared-memory ring:
                                4 (default for max_rows 16): 4 x 3-stage rings; 2: 2 x 6; 1: 1 x 12
-                               (deeper rings stream faster per item: small batches)              */
+                               (deeper rings stream faster per item: small batches).  32-row
+                               items use 4 teams of 2 warps (one per 16-row tile, each taking
+                               every page of a stage; fp8 pools: 2 teams of 4).  Must be 0 with
+                               max_rows 0.                                                       */
 } spa_plan_config;
 
 /* cfg may be NULL (defaults).  The plan keeps a pointer to `pool`. */

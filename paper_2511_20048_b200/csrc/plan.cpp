@@ -48,43 +48,55 @@ using namespace spa;
 
 extern "C" {
 
+// Kernel geometry of a plan with `mt` 16-row tiles per item: teams per CTA and key-split
+// warps per row tile.  32-row items take one warp per row tile over every page of a stage
+// (kw 1, 4 teams: measured 1.4x the key-split layout at k = 3, profiles/r02_*); fp8 pools
+// keep the key-split layout (the only fp8 instantiation).
+static spa_status set_geometry(spa_plan* P, int mt, int teams_req) {
+    P->mt = mt;
+    int teams = teams_req;
+    if (const char* e = std::getenv("SPA_TEAMS")) teams = std::atoi(e);
+    int kw = mt == 2 && !P->pool->kv_fp8 ? 1 : 2;
+    if (const char* e = std::getenv("SPA_KW")) kw = std::atoi(e) == 1 && mt == 2 && !P->pool->kv_fp8 ? 1 : 2;
+    if (teams == 0) teams = kw == 1 ? 4 : mt == 1 ? 4 : mt == 2 ? 2 : 1;
+    if (!decode_teams_supported(mt, teams, kw))
+        return fail(SPA_ERR_UNSUPPORTED, "teams_per_cta must be 1, 2 or 4 (4 only with max_rows 16 or 32, 1 with 64)");
+    P->teams = teams;
+    P->kw = kw;
+    P->n_teams = P->num_ctas * teams;
+    return SPA_OK;
+}
+
 spa_status spa_plan_create(spa_pool* pool, const spa_plan_config* cfg, spa_plan** out) {
     if (!pool || !out) return fail(SPA_ERR_INVALID_ARG, "null argument");
     *out = nullptr;
     spa_plan_config c{};
     c.sharing = 1;
     if (cfg) c = *cfg;
-    if (c.max_rows == 0) c.max_rows = 16;
-    if (c.max_rows != 16 && c.max_rows != 32 && c.max_rows != 64 && c.max_rows != 128)
-        return fail(SPA_ERR_UNSUPPORTED, "max_rows must be 16, 32, 64 or 128");
+    if (c.max_rows != 0 && c.max_rows != 16 && c.max_rows != 32 && c.max_rows != 64 && c.max_rows != 128)
+        return fail(SPA_ERR_UNSUPPORTED, "max_rows must be 0 (auto), 16, 32, 64 or 128");
     if (c.max_rows == 128 && !ext_supported(pool->cfg.head_dim))
         return fail(SPA_ERR_UNSUPPORTED, "max_rows 128 (tcgen05 extend kernel) needs head_dim 128");
     if (c.split_pages < 0 || c.num_ctas < 0) return fail(SPA_ERR_INVALID_ARG, "negative plan option");
     if (c.merge_mode < 0 || c.merge_mode > 2) return fail(SPA_ERR_INVALID_ARG, "merge_mode must be 0, 1 or 2");
+    if (c.max_rows == 0 && c.teams_per_cta != 0)
+        return fail(SPA_ERR_INVALID_ARG, "max_rows 0 (auto) chooses teams_per_cta itself: pass 0");
     const int G = pool->cfg.num_q_heads / pool->cfg.num_kv_heads;
-    if (G > c.max_rows) return fail(SPA_ERR_UNSUPPORTED, "GQA group size exceeds max_rows");
+    if (G > (c.max_rows ? c.max_rows : 32)) return fail(SPA_ERR_UNSUPPORTED, "GQA group size exceeds max_rows");
+    if (c.max_rows == 128 && c.merge_mode != 2 && c.merge_mode != 0)
+        return fail(SPA_ERR_UNSUPPORTED, "max_rows 128 merges split partials with the merge kernel");
     spa_plan* P = new spa_plan();
     P->pool = pool;
     P->cfg = c;
-    P->mt = c.max_rows / 16;
+    P->auto_rows = c.max_rows == 0;
     int ctas = c.num_ctas;
     if (ctas == 0) ctas = pool->sm_count > 0 ? pool->sm_count : 148;
     P->num_ctas = ctas;
-    int teams = c.teams_per_cta;
-    if (const char* e = std::getenv("SPA_TEAMS")) teams = std::atoi(e);
-    // 32-row items: SPA_KW=1 selects one warp per row tile over every page of a stage
-    int kw = 2;
-    if (const char* e = std::getenv("SPA_KW")) kw = std::atoi(e) == 1 && P->mt == 2 ? 1 : 2;
-    if (teams == 0) teams = kw == 1 ? 4 : P->mt == 1 ? 4 : P->mt == 2 ? 2 : 1;
-    if (P->mt == 8 && c.merge_mode != 2 && c.merge_mode != 0)
-        return fail(SPA_ERR_UNSUPPORTED, "max_rows 128 merges split partials with the merge kernel");
-    if (!decode_teams_supported(P->mt, teams, kw)) {
+    const int mt = c.max_rows ? c.max_rows / 16 : (G > 16 ? 2 : 1);
+    if (spa_status st = set_geometry(P, mt, c.teams_per_cta)) {
         delete P;
-        return fail(SPA_ERR_UNSUPPORTED, "teams_per_cta must be 1, 2 or 4 (4 only with max_rows 16, 1 with 64)");
+        return st;
     }
-    P->teams = teams;
-    P->kw = kw;
-    P->n_teams = ctas * teams;
     *out = P;
     return SPA_OK;
 }
@@ -214,7 +226,6 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
             groups[ins.first->second].push_back(i);
         }
     }
-    const int max_members = std::max(1, P->cfg.max_rows / G);
 
     // ---- 2. ranges: a prefix tree of page-id runs per group (reading #18).  Sharing is
     //      positional and prefix-shaped, so over page index k the requests of a group that
@@ -225,7 +236,7 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
     //      speculative prompt read once by the k samples forked from it (PAPER.md:189, :198,
     //      :335; nested forks, reading #17), each request's private tail by its own rows.
     //      A class with more than max_rows / G rows is cut into chunks that re-read it.
-    std::vector<Range> ranges;
+    std::vector<Range> ranges, classes;   // classes: one per prefix-tree run, before max_rows chunking
     int n_groups = 0;
     int64_t unique_tokens = 0, unshared_tokens = 0;
     for (int i = 0; i < n_req; ++i) unshared_tokens += V[i].hi - lo[i];
@@ -356,11 +367,31 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
                 for (int x = ufirst[u]; x < urow_end[u]; ++x)
                     if (lo[x] < b && V[x].hi > a) rows.push_back(x);
             std::sort(rows.begin(), rows.end());
-            for (size_t c0 = 0; c0 < rows.size(); c0 += max_members) {
-                std::vector<int> chunk(rows.begin() + c0, rows.begin() + std::min(rows.size(), c0 + max_members));
-                // chunk rows may span requests: the page list is the same for all of them
-                ranges.push_back(Range{r.reqs.size() > 1 ? 0 : 1, gid, std::move(chunk), a, b, &table(r.reqs[0])});
-            }
+            classes.push_back(Range{r.reqs.size() > 1 ? 0 : 1, gid, std::move(rows), a, b, &table(r.reqs[0])});
+        }
+    }
+
+    // max_rows 0 (auto): 32-row items when classes of more than 16 rows (k = 3 forks of a
+    // Qwen context: 4 x G = 20 rows) hold a large share of the pages, so each
+    // is read once by one item instead of twice by 16-row chunks; else 16-row items
+    if (P->auto_rows) {
+        int64_t pages_all = 0, pages_big = 0;
+        for (const auto& c : classes) {
+            const int64_t np = cdiv(c.b, ps) - c.a / ps;
+            pages_all += np;
+            if (int64_t(c.members.size()) * G > 16) pages_big += np;
+        }
+        const int mt = G > 16 || (!pool->kv_fp8 && pages_big * 10 > pages_all * 3) ? 2 : 1;
+        if (mt != P->mt)
+            if (spa_status st = set_geometry(P, mt, 0)) return st;
+    }
+    const int max_members = std::max(1, P->mt * 16 / G);
+    for (auto& c : classes) {
+        for (size_t c0 = 0; c0 < c.members.size(); c0 += max_members) {
+            std::vector<int> chunk(c.members.begin() + c0,
+                                   c.members.begin() + std::min(c.members.size(), c0 + max_members));
+            // chunk rows may span requests: the page list is the same for all of them
+            ranges.push_back(Range{c.kind, c.group, std::move(chunk), c.a, c.b, c.table});
         }
     }
 

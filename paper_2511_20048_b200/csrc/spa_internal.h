@@ -109,6 +109,7 @@ struct spa_plan {
     int mt = 1;                 // m16 tiles (warps) per team: max_rows / 16
     int teams = 4;              // teams (work-item streams with private rings) per CTA
     int kw = 2;                 // key-split warps per row tile (1: a warp takes every page of a stage)
+    bool auto_rows = false;     // max_rows 0: 16- or 32-row items chosen per batch (spa_decode_plan)
     int n_teams = 0;
     int num_ctas = 0;
     // host view of the last plan

@@ -342,9 +342,10 @@ class Pool:
 
 
 class Plan:
-    def __init__(self, pool: Pool, sharing=True, max_rows=16, split_pages=0, num_ctas=0, merge_mode=0,
+    def __init__(self, pool: Pool, sharing=True, max_rows=0, split_pages=0, num_ctas=0, merge_mode=0,
                  teams_per_cta=0):
-        """merge_mode: 0 in-kernel tail phase (default), 1 in-kernel last arriver, 2 merge kernel."""
+        """max_rows: 0 auto (16 or 32 rows per item, per batch), 16, 32, 64, 128.
+        merge_mode: 0 in-kernel tail phase (default), 1 in-kernel last arriver, 2 merge kernel."""
         self.pool = pool
         cfg = spa_plan_config(1 if sharing else 0, max_rows, split_pages, num_ctas, int(merge_mode), int(teams_per_cta))
         h = c_void_p()

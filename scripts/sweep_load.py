@@ -47,11 +47,9 @@ def main():
     # one pool for every point: sized for the largest batch
     pages = max(bench.pages_for(workloads.sweep(b, f), 8) for b in batches for f in fracs)
     pool = spa.Pool(Lr, m.num_q_heads, m.num_kv_heads, m.head_dim, pages, device=dev)
-    plans = {"shared": spa.Plan(pool), "shared32": spa.Plan(pool, max_rows=32)}
-    os.environ["SPA_KW"] = "1"          # 32-row items, one warp per row tile, no key split
-    plans["shared32kw1"] = spa.Plan(pool, max_rows=32)
-    del os.environ["SPA_KW"]
-    plans["unshared"] = spa.Plan(pool, sharing=False)
+    # shared: the library default (max_rows 0: 16- or 32-row items chosen per batch)
+    plans = {"shared": spa.Plan(pool), "shared16": spa.Plan(pool, max_rows=16),
+             "shared32": spa.Plan(pool, max_rows=32), "unshared": spa.Plan(pool, sharing=False)}
     if a.plans:
         plans = {k: v for k, v in plans.items() if k in a.plans.split(",")}
     rows = []
@@ -91,7 +89,7 @@ def main():
                                 "alg_gbs": ab / (layer_ms * 1e-3) / 1e9, "alg_tokens_per_head": st["alg_tokens"],
                                 "read_tokens_per_head": st["unique_tokens"],
                                 "overhead_bytes": bench.overhead_bytes(st, m.num_kv_heads, m.num_q_heads, m.head_dim),
-                                "records": st["n_records"]}
+                                "records": st["n_records"], "rows_max": st["rows_max"]}
             rows.append(rec_row)
             out.write(json.dumps(rec_row) + "\n")
             out.flush()
