@@ -17,8 +17,11 @@
  *
  * Conventions
  *  - All device memory named in these signatures is caller-owned (PyTorch allocates it)
- *    unless stated otherwise; the library owns host metadata (request table, page
- *    tables, refcounts, free set, plans) and a plan's own small device buffers.
+ *    unless stated otherwise: the KV pools, q/o/lse, new K/V and the plan workspace
+ *    (spa_plan_set_workspace) -- the plan path never calls cudaMalloc/cudaFree.  The library
+ *    owns host metadata (request table, page tables, refcounts, free set, plans, a plan's
+ *    pinned host staging buffer).  Exceptions, stated at their calls: the F1 peer regions
+ *    (spa_peer_create, shared over CUDA IPC) and NCCL's own buffers.
  *  - bf16 means IEEE bfloat16 bit patterns (uint16).  Strides are in ELEMENTS.
  *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Device work is
  *    stream-ordered; host metadata changes take effect when the call returns.
@@ -48,7 +51,9 @@ typedef enum spa_status {
     SPA_ERR_CUDA = 4,          /* a CUDA runtime/driver call or kernel failed (see spa_last_error) */
     SPA_ERR_NCCL = 5,          /* NCCL could not be loaded or a collective failed */
     SPA_ERR_UNSUPPORTED = 6,   /* configuration the kernels do not implement (head_dim, page_size, ...) */
-    SPA_ERR_NO_DEVICE = 7      /* device work requested from a metadata-only pool */
+    SPA_ERR_NO_DEVICE = 7,     /* device work requested from a metadata-only pool */
+    SPA_ERR_WORKSPACE = 8      /* the plan's caller-owned workspace is missing or too small
+                                  (spa_plan_workspace_size gives the bytes needed) */
 } spa_status;
 
 typedef int64_t spa_req;                 /* request id: 1, 2, 3, ... never reused (reading #4) */
@@ -187,12 +192,27 @@ typedef struct spa_plan_config {
 spa_status spa_plan_create(spa_pool* pool, const spa_plan_config* cfg, spa_plan** out);
 spa_status spa_plan_destroy(spa_plan* plan);
 
+/* Caller-owned plan workspace (all device memory is caller-owned).
+ * Device memory, 256-B aligned, that holds the uploaded plan (queue, descriptors, page list,
+ * merge counters) followed by the split partials (fp32 O [records][Hq][d], fp32 LSE).  Set
+ * it before planning; spa_decode_plan / spa_extend_plan never allocate device memory.  A
+ * plan that needs more than `bytes` fails with SPA_ERR_WORKSPACE (nothing is enqueued and
+ * decode launches are refused until a plan succeeds); spa_plan_workspace_size then returns
+ * the bytes that plan needs (after any plan call: the last plan's need), so the caller can
+ * grow the buffer and plan again.  Changing the pointer invalidates the uploaded plan (plan
+ * again) and bumps spa_plan_stats.generation (CUDA graphs captured over the old pointer are
+ * stale).  The workspace must stay allocated while launches that use it are in flight.
+ * Graph capture: a plan call on a capturing stream records the upload as a memcpy node
+ * (from the plan's pinned staging buffer, which must already be large enough: plan the
+ * same batch once before capturing), so replaying plan + decode launches is consistent. */
+spa_status spa_plan_set_workspace(spa_plan* plan, void* workspace, size_t bytes);
+spa_status spa_plan_workspace_size(const spa_plan* plan, size_t* out_bytes);
+
 /* (Re)plan a decode batch: reqs[0..n_req) (host), all of length >= 1, no duplicates.
  *   window > 0: sliding window, request r attends to keys [max(0, n_r - window), n_r)
  *   (reading #9); window <= 0: full attention.  Batch row i of q/o/lse below is reqs[i].
- *   The plan's metadata is uploaded to its device buffers on `stream`; device buffers
- *   only grow (spa_plan_stats.generation changes when they move, which invalidates CUDA
- *   graphs captured over this plan). */
+ *   The plan's metadata is uploaded into the caller's workspace on `stream` (above);
+ *   SPA_ERR_WORKSPACE if it does not fit. */
 spa_status spa_decode_plan(spa_plan* plan, int32_t n_req, const spa_req* reqs, int32_t window, void* stream);
 
 /* (Re)plan an EXTEND batch (the prefill of a speculative prompt

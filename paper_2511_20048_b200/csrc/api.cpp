@@ -24,6 +24,8 @@ static spa_status check_decode_args(const spa_plan* plan, int32_t layer, const v
     if (pool->metadata_only) return fail(SPA_ERR_NO_DEVICE, "decode on a metadata-only pool");
     if (spa_status s = check_device(pool)) return s;
     if (plan->host.empty()) return fail(SPA_ERR_INVALID_ARG, "plan has not been built (spa_decode_plan)");
+    if (!plan->uploaded)
+        return fail(SPA_ERR_WORKSPACE, "the last spa_decode_plan did not reach the device (no or too small workspace)");
     if (layer < 0 || layer >= pool->cfg.num_layers) return fail(SPA_ERR_INVALID_ARG, "layer out of range");
     if (plan->n_req > 0 && (!q || !o)) return fail(SPA_ERR_INVALID_ARG, "null q or o");
     // 32-bit query loads and bf16x2 output stores need even element strides and 4-B alignment

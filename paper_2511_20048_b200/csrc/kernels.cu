@@ -317,58 +317,67 @@ int launch_merge(int32_t n_req, int32_t num_heads, int32_t head_dim, const int32
 }
 
 // ============================================================================ plan device buffers
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+size_t plan_workspace_need(const spa_plan* P) {
+    const auto& c = P->pool->cfg;
+    const size_t records = size_t(P->host[H_N_RECORDS]);
+    return align256(P->host.size() * 4) + align256(records * c.num_q_heads * c.head_dim * 4) +
+           records * c.num_q_heads * 4;
+}
+
+// Upload the host plan into the caller's workspace (S8(b): all device memory is caller-owned).
+// Returns kUploadNoWorkspace when the workspace is missing or too small (nothing enqueued),
+// else a cudaError_t.  Under stream capture the upload becomes a memcpy node that re-reads
+// the pinned staging buffer at every replay (which also re-zeroes the queue and merge
+// counters, so a captured plan + its decode launches replay consistently); no event is
+// waited on or recorded then, and the staging buffer must already be large enough.
 int plan_upload(spa_plan* P, void* stream) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaError_t e = cudaSuccess;
-    if (!P->upload_event) {
+    P->ws_need = plan_workspace_need(P);
+    if (!P->ws || P->ws_need > P->ws_bytes) return kUploadNoWorkspace;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    e = cudaStreamIsCapturing(s, &cap);
+    if (e) return int(e);
+    const bool capturing = cap != cudaStreamCaptureStatusNone;
+    if (!capturing && !P->upload_event) {
         cudaEvent_t ev;
         e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
         if (e) return int(e);
         P->upload_event = ev;
     }
-    if (P->upload_pending) {   // the pinned staging buffer may still be read by the last upload
+    if (!capturing && P->upload_pending) {   // the pinned staging buffer may still be read by the last upload
         e = cudaEventSynchronize(static_cast<cudaEvent_t>(P->upload_event));
         if (e) return int(e);
         P->upload_pending = false;
     }
     const size_t words = P->host.size();
-    if (words > P->pinned_words) {
+    if (words > P->pinned_words) {   // host staging memory (library-owned host metadata)
+        if (capturing) return int(cudaErrorStreamCaptureUnsupported);
         if (P->pinned) cudaFreeHost(P->pinned);
         P->pinned = nullptr;
+        P->pinned_words = 0;
         const size_t nw = words + words / 2 + 1024;
         e = cudaMallocHost(reinterpret_cast<void**>(&P->pinned), nw * 4);
         if (e) return int(e);
         P->pinned_words = nw;
     }
     std::memcpy(P->pinned, P->host.data(), words * 4);
-    if (words > P->d_meta_words) {
-        if (P->d_meta) cudaFree(P->d_meta);
-        P->d_meta = nullptr;
-        const size_t nw = words + words / 2 + 1024;
-        e = cudaMalloc(reinterpret_cast<void**>(&P->d_meta), nw * 4);
-        if (e) return int(e);
-        P->d_meta_words = nw;
-        P->generation++;
-    }
+    const auto& c = P->pool->cfg;
     const size_t records = size_t(P->host[H_N_RECORDS]);
-    if (records > P->part_records) {
-        const auto& c = P->pool->cfg;
-        if (P->d_part_o) cudaFree(P->d_part_o);
-        if (P->d_part_lse) cudaFree(P->d_part_lse);
-        P->d_part_o = nullptr;
-        P->d_part_lse = nullptr;
-        const size_t nr = records + records / 4 + 64;
-        e = cudaMalloc(reinterpret_cast<void**>(&P->d_part_o), nr * c.num_q_heads * c.head_dim * 4);
-        if (!e) e = cudaMalloc(reinterpret_cast<void**>(&P->d_part_lse), nr * c.num_q_heads * 4);
-        if (e) return int(e);
-        P->part_records = nr;
-        P->generation++;
-    }
+    char* base = static_cast<char*>(P->ws);
+    P->d_meta = reinterpret_cast<int32_t*>(base);
+    P->d_part_o = reinterpret_cast<float*>(base + align256(words * 4));
+    P->d_part_lse = reinterpret_cast<float*>(base + align256(words * 4) +
+                                             align256(records * c.num_q_heads * c.head_dim * 4));
     e = cudaMemcpyAsync(P->d_meta, P->pinned, words * 4, cudaMemcpyHostToDevice, s);
     if (e) return int(e);
-    e = cudaEventRecord(static_cast<cudaEvent_t>(P->upload_event), s);
-    if (e) return int(e);
-    P->upload_pending = true;
+    if (!capturing) {
+        e = cudaEventRecord(static_cast<cudaEvent_t>(P->upload_event), s);
+        if (e) return int(e);
+        P->upload_pending = true;
+    }
     return 0;
 }
 
@@ -378,9 +387,6 @@ void plan_release(spa_plan* P) {
         cudaEventDestroy(static_cast<cudaEvent_t>(P->upload_event));
     }
     if (P->pinned) cudaFreeHost(P->pinned);
-    if (P->d_meta) cudaFree(P->d_meta);
-    if (P->d_part_o) cudaFree(P->d_part_o);
-    if (P->d_part_lse) cudaFree(P->d_part_lse);
     P->upload_event = nullptr;
     P->pinned = nullptr;
     P->d_meta = nullptr;

@@ -641,9 +641,16 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
     P->window = window;
     P->n_req = n_req;
 
+    P->uploaded = false;
+    P->ws_need = plan_workspace_need(P);
     if (!pool->metadata_only) {
         int err = plan_upload(P, stream);
+        if (err == kUploadNoWorkspace)
+            return fail(SPA_ERR_WORKSPACE, "plan workspace missing or too small: " + std::to_string(P->ws_need) +
+                                               " bytes needed, " + std::to_string(P->ws_bytes) +
+                                               " set (spa_plan_workspace_size / spa_plan_set_workspace)");
         if (err) return fail(SPA_ERR_CUDA, std::string("plan upload: ") + cuda_error_string(err));
+        P->uploaded = true;
     }
     st.generation = P->generation;
     return SPA_OK;
@@ -652,6 +659,25 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
 }  // namespace
 
 extern "C" {
+
+spa_status spa_plan_set_workspace(spa_plan* plan, void* workspace, size_t bytes) {
+    if (!plan) return fail(SPA_ERR_INVALID_ARG, "null plan");
+    if (!workspace && bytes) return fail(SPA_ERR_INVALID_ARG, "null workspace with nonzero size");
+    if (reinterpret_cast<uintptr_t>(workspace) & 255) return fail(SPA_ERR_INVALID_ARG, "workspace must be 256-B aligned");
+    if (workspace != plan->ws || bytes < plan->ws_need) {   // the built plan's device copy moves or no longer fits
+        if (workspace != plan->ws) plan->generation++;
+        plan->uploaded = false;
+    }
+    plan->ws = workspace;
+    plan->ws_bytes = workspace ? bytes : 0;
+    return SPA_OK;
+}
+
+spa_status spa_plan_workspace_size(const spa_plan* plan, size_t* out_bytes) {
+    if (!plan || !out_bytes) return fail(SPA_ERR_INVALID_ARG, "null argument");
+    *out_bytes = plan->host.size() >= size_t(H_WORDS) ? plan->ws_need : 0;
+    return SPA_OK;
+}
 
 spa_status spa_plan_get_stats(const spa_plan* plan, spa_plan_stats* out) {
     if (!plan || !out) return fail(SPA_ERR_INVALID_ARG, "null argument");

@@ -119,12 +119,15 @@ struct spa_plan {
     size_t pinned_words = 0;
     void* upload_event = nullptr;  // cudaEvent_t
     bool upload_pending = false;
-    // device buffers (grow only)
+    // caller-owned device workspace (spa_plan_set_workspace): plan metadata, then the split
+    // partials (fp32 O, then LSE), each 256-B aligned; the library never allocates device memory
+    void* ws = nullptr;
+    size_t ws_bytes = 0;
+    size_t ws_need = 0;         // bytes the last built plan needs (also after SPA_ERR_WORKSPACE)
+    bool uploaded = false;      // the last built plan is on the device (decode launches allowed)
     int32_t* d_meta = nullptr;
-    size_t d_meta_words = 0;
     float* d_part_o = nullptr;
     float* d_part_lse = nullptr;
-    size_t part_records = 0;
     int generation = 0;
     spa_plan_stats stats{};
     int32_t window = 0;
@@ -133,6 +136,11 @@ struct spa_plan {
     unsigned long long* trace = nullptr;   // spa_debug_set_trace: timeline buffer (device), or null
     int32_t trace_cap = 0;
 };
+
+namespace spa {
+constexpr int kUploadNoWorkspace = -1;   // plan_upload: workspace missing or too small
+size_t plan_workspace_need(const spa_plan* P);
+}  // namespace spa
 
 struct spa_comm {
     void* nccl_comm = nullptr;

@@ -19,7 +19,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, os.path.basename(os.environ.get("SPA_LIB", "libspa.so")))
 
 SPA_OK, SPA_ERR_INVALID_ARG, SPA_ERR_NO_PAGES, SPA_ERR_BAD_REQUEST = 0, 1, 2, 3
-SPA_ERR_CUDA, SPA_ERR_NCCL, SPA_ERR_UNSUPPORTED, SPA_ERR_NO_DEVICE = 4, 5, 6, 7
+SPA_ERR_CUDA, SPA_ERR_NCCL, SPA_ERR_UNSUPPORTED, SPA_ERR_NO_DEVICE, SPA_ERR_WORKSPACE = 4, 5, 6, 7, 8
 
 c_int32, c_int64, c_void_p, c_float = ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_float
 P_int32 = ctypes.POINTER(c_int32)
@@ -68,6 +68,8 @@ _SIGS = {
     "spa_decode_plan": (c_int32, [c_void_p, c_int32, P_int64, c_int32, c_void_p]),
     "spa_extend_plan": (c_int32, [c_void_p, c_int32, P_int64, P_int32, c_int32, c_void_p]),
     "spa_plan_get_stats": (c_int32, [c_void_p, ctypes.POINTER(spa_plan_stats)]),
+    "spa_plan_set_workspace": (c_int32, [c_void_p, c_void_p, ctypes.c_size_t]),
+    "spa_plan_workspace_size": (c_int32, [c_void_p, ctypes.POINTER(ctypes.c_size_t)]),
     "spa_decode_attention": (c_int32, [c_void_p, c_int32, c_void_p, c_int64, c_int64, c_void_p, c_int64, c_int64,
                                        c_void_p, c_int64, c_int64, c_float, c_void_p]),
     "spa_merge_splits": (c_int32, [c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_int64,
@@ -343,15 +345,31 @@ class Pool:
 
 class Plan:
     def __init__(self, pool: Pool, sharing=True, max_rows=0, split_pages=0, num_ctas=0, merge_mode=0,
-                 teams_per_cta=0):
+                 teams_per_cta=0, workspace=None):
         """max_rows: 0 auto (16 or 32 rows per item, per batch), 16, 32, 64, 128.
-        merge_mode: 0 in-kernel tail phase (default), 1 in-kernel last arriver, 2 merge kernel."""
+        merge_mode: 0 in-kernel tail phase (default), 1 in-kernel last arriver, 2 merge kernel.
+        workspace: a caller-owned uint8 device tensor for the plan (include/spa.h
+        spa_plan_set_workspace), fixed; None = a torch tensor this object grows on demand."""
         self.pool = pool
         cfg = spa_plan_config(1 if sharing else 0, max_rows, split_pages, num_ctas, int(merge_mode), int(teams_per_cta))
         h = c_void_p()
         _check(lib().spa_plan_create(pool.h, ctypes.byref(cfg), ctypes.byref(h)))
         self.h = h
         self.n_req = 0
+        self._ws = None
+        self._ws_fixed = workspace is not None
+        if workspace is not None:
+            self.set_workspace(workspace)
+
+    def set_workspace(self, ws):
+        """Hand the plan a caller-owned device workspace (uint8 tensor, 256-B aligned)."""
+        self._ws = ws
+        _check(lib().spa_plan_set_workspace(self.h, _ptr(ws), ws.numel() * ws.element_size()))
+
+    def workspace_size(self) -> int:
+        n = ctypes.c_size_t()
+        _check(lib().spa_plan_workspace_size(self.h, ctypes.byref(n)))
+        return n.value
 
     def close(self):
         if self.h:
@@ -380,6 +398,15 @@ class Plan:
             qa = (c_int32 * max(n, 1))(*[int(x) for x in n_query])
             st = lib().spa_extend_plan(self.h, n, ra, qa, int(window), sp)
             rows = int(sum(int(x) for x in n_query))
+        if st == SPA_ERR_WORKSPACE and not self._ws_fixed:
+            import torch  # noqa: WPS433
+
+            need = self.workspace_size()
+            self.set_workspace(torch.empty(need + need // 2 + 4096, dtype=torch.uint8, device=self.pool.k.device))
+            if n_query is None:
+                st = lib().spa_decode_plan(self.h, n, ra, int(window), sp)
+            else:
+                st = lib().spa_extend_plan(self.h, n, ra, qa, int(window), sp)
         if check:
             _check(st)
             self.n_req = rows

@@ -68,7 +68,7 @@ def _worker(rank, world, port, q):
         wdig = [None] * world
         dist.all_gather_object(wdig, _state_digest(pool, plan, reqs))
         digests = [a + b for a, b in zip(digests, wdig)]
-        uid = [os.urandom(128) if rank == 0 else None]   # stands in for spa_nccl_unique_id()
+        uid = [spa.spa_nccl_unique_id() if rank == 0 else None]   # the real NCCL bootstrap id (no GPU needed)
         dist.broadcast_object_list(uid, src=0)
         uids = [None] * world
         dist.all_gather_object(uids, uid[0])
