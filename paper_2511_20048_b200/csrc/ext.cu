@@ -8,21 +8,29 @@
 // M = 128 rows, fp32 accumulators in tensor memory.
 //
 // One CTA per SM, warp-specialised:
-//   warp 0      producer: pops items from the plan's dynamic queue and streams each stage
-//               (4 pages = 64 keys of K and V of one KV head, 32 KB) into a 5-stage
-//               shared-memory ring (TMA: K chunk by chunk so a stage's keys are contiguous,
-//               V one box per page);
-//   warp 1      MMA issuer (one elected lane): S_j = Q K_j^T (8 x M128 N64 K16, A = the
-//               item's Q tile, K-major SW128; B = the stage's keys), then
-//               O += P_{j-1} V_{j-1} (per page: M128 N128 K16, A = P in tensor memory,
-//               B = the V page as an MN-major SW128 operand);
+//   warp 0      K producer: pops items from the plan's dynamic queue and streams each stage's
+//               keys (4 pages = 64 keys of one KV head, 16 KB, chunk by chunk so a stage's keys
+//               are contiguous) into the K ring, one TMA box per lane;
+//   warp 10     V producer: follows the K producer's items, streams the stage's V pages (one
+//               box per page and lane) into the V ring.  The rings are separate because K is
+//               consumed by S_j and freed as soon as that MMA completes, while V waits for P_j
+//               (PV lags S by two stages); the two producers and the per-lane boxes exist
+//               because one issuing thread cannot keep enough TMA traffic in flight
+//               (scripts/micro/tma_rate.cu);
+//   warp 1      S issuer (one elected lane): S_j = Q K_j^T (8 x M128 N64 K16, A = the item's Q
+//               tile in tensor memory; B = the stage's keys, K-major SW128);
+//   warp 12     PV issuer: O += P_j V_j (per page: M128 N128 K16, A = P in tensor memory,
+//               B = the V page as an MN-major SW128 operand).  Two issuers because a thread's
+//               tcgen05.mma issue blocks while the tensor pipe works: one issuer serialised S
+//               and PV (measured: ~0.6 us of issue per 64-key stage);
 //   warps 2-9   two softmax warpgroups, one thread per query row (tensor-memory lane) each;
 //               WG k takes the stages of parity k: loads S, masks (window lo, causal hi,
 //               range end), runs the online softmax in the log2 domain with lazy rescaling
 //               (threshold 2^8) of its own accumulator O_k in tensor memory, writes P (bf16)
 //               over S's columns; at item end the two (m, l, O_k) merge per row and bf16 O +
 //               LSE (or an fp32 partial record for split ranges) are written.
-// Tensor memory: S buffers 0-3 (64 columns each; PV lags S by 2 stages), O_0, O_1 (128 each).
+// Tensor memory: S buffers 0-2 (64 columns each; PV lags S by 2 stages), the Q tile (64 columns:
+// the A operand of S = Q K^T, so S reads only K from shared memory), O_0, O_1 (128 each).
 #include "device_util.cuh"
 #include "spa_internal.h"
 #include "umma.cuh"
@@ -76,10 +84,14 @@ struct ExtParams {
 };
 
 struct ExtItem {
-    int it, kv_head, n_pages, tok_start, tok_end, member_off, n_members, kind;
+    int it, kv_head, n_pages, tok_start, tok_end, member_off, n_members, kind, page_off;
 };
 
 namespace ext {
+#ifndef SPA_EXT_EXP
+#define SPA_EXT_EXP 0   // timing experiments (wrong results by design): 1 no MMAs, 2 no softmax math
+#endif
+constexpr int EXP = SPA_EXT_EXP;
 constexpr int D = 128;
 constexpr int PAGE_BYTES = kPageSize * D * 2;     // 4 KB: K (or V) of one page, one head
 #ifndef SPA_EXT_PPS
@@ -87,29 +99,46 @@ constexpr int PAGE_BYTES = kPageSize * D * 2;     // 4 KB: K (or V) of one page,
 #endif
 constexpr int PPS = SPA_EXT_PPS;                  // pages per stage
 constexpr int KPS = PPS * kPageSize;              // keys per stage (S columns)
-constexpr int STAGE_BYTES = PPS * 2 * PAGE_BYTES; // PPS pages x (K, V)
-// stage layout: K key-contiguous [2 chunks][KPS rows][128 B] (one MMA covers every key of the
-// stage: N = KPS), then V page by page [page][2 chunks][16 rows][128 B] (one K=16 MMA each)
+static_assert(32 % PPS == 0, "producers refresh page ids per 32-page window");
+constexpr int HALF_BYTES = PPS * PAGE_BYTES;      // K (or V) of one stage
+// K stage: key-contiguous [2 chunks][KPS rows][128 B] (one MMA covers every key of the stage:
+// N = KPS); V stage: page by page [page][2 chunks][16 rows][128 B] (one K=16 MMA each)
 constexpr int K_CHUNK = KPS * 128;                // bytes per 64-column chunk of the stage's keys
-constexpr int OFF_V = 2 * K_CHUNK;
-constexpr int NS = (232448 - 1024 - 32768 - 4096) / STAGE_BYTES;   // ring stages
-constexpr int QN = NS + 8;   // popped-item queue entries: the producer runs up to NS + LAG + 1
-                              // stages (items, when items are one stage long) ahead of the WGs
-constexpr int OFF_Q = NS * STAGE_BYTES;           // Q tile: 2 chunks x 128 rows x 128 B
-constexpr int OFF_BAR = OFF_Q + 32768;
-// barriers: full[NS], empty[NS], s_full[4], p_full[4] (one per S buffer: a buffer's next
-// S / P needs this round's P / S, so each barrier is at most one phase ahead of its waiter),
-// q_ready, o_full, pv_done[4] (PV of the stages using S buffer b)
-constexpr int BAR_FULL = 0, BAR_EMPTY = NS, BAR_SFULL = 2 * NS, BAR_PFULL = 2 * NS + 4, BAR_QREADY = 2 * NS + 8,
-              BAR_OFULL = 2 * NS + 9, BAR_PVDONE = 2 * NS + 10, N_BARS = 2 * NS + 14;
+constexpr int N_SLOTS = (232448 - 1024 - 4096) / HALF_BYTES;   // 16-KB ring slots (Q lives in tensor memory)
+#ifndef SPA_EXT_NK
+#define SPA_EXT_NK 4
+#endif
+constexpr int NK = SPA_EXT_NK;                    // K ring stages (held from TMA issue to S_j done)
+constexpr int NV = N_SLOTS - NK;                  // V ring stages (held until PV_j, after P_j)
+static_assert(NK >= 2 && NV >= 3, "ring depths");
+constexpr int QN = NV + 12;  // popped-item queue entries: the leader runs at most NK + 3 stages
+                             // (items, when items are one stage long) ahead of the PV issuer
+constexpr int OFF_V = NK * HALF_BYTES;
+constexpr int OFF_BAR = (NK + NV) * HALF_BYTES;
+// barriers: kfull[NK], kempty[NK], vfull[NV], vempty[NV], s_full[4], p_full[4] (one per S
+// buffer: a buffer's next S / P needs this round's P / S, so each barrier is at most one phase
+// ahead of its waiter; 3 of the 4 are used), q_ready, o_full, pv_done[4] (PV of the stages
+// using S buffer b)
+constexpr int BAR_KFULL = 0, BAR_KEMPTY = NK, BAR_VFULL = 2 * NK, BAR_VEMPTY = 2 * NK + NV,
+              BAR_SFULL = 2 * (NK + NV), BAR_PFULL = BAR_SFULL + 4, BAR_QREADY = BAR_SFULL + 8,
+              BAR_OFULL = BAR_SFULL + 9, BAR_PVDONE = BAR_SFULL + 10, N_BARS = BAR_SFULL + 14;
 constexpr int OFF_TQ = OFF_BAR + N_BARS * 8;
-constexpr int OFF_ML = (OFF_TQ + QN * int(sizeof(ExtItem)) + 15) & ~15;   // [2][2][128] fp32 + 8 flags
+constexpr int OFF_TSEQ = OFF_TQ + QN * int(sizeof(ExtItem));   // int[QN]: entry n published as n + 1
+constexpr int OFF_ML = (OFF_TSEQ + QN * 4 + 15) & ~15;           // [2][2][128] fp32 + 8 flags
 constexpr int OFF_TSLOT = OFF_ML + 4 * 128 * 4 + 8 * 4;
 constexpr int SMEM = 1024 + OFF_TSLOT + 16 + 128;   // + debug words (hang-trap builds)
-constexpr int THREADS = 320;                       // producer, MMA issuer, 2 softmax warpgroups
+constexpr int KW = 2;   // K producer warps (one 64-channel chunk each)
+// warps: 0 K producer (chunk 0, pops items), 1 S issuer, 2-9 softmax warpgroups, 10 V producer,
+// 11 K producer (chunk 1), 12 PV issuer
+constexpr int THREADS = 13 * 32;
+constexpr int WARP_V = 10, WARP_K1 = 11, WARP_PV = 12;
 // tensor memory: S buffers 0..3 (KPS columns each; stage g uses g % 4), O_0, O_1 (128 each)
-constexpr uint32_t TMEM_COLS = 512, S_COL = 0, O_COL = 256;
-static_assert(4 * KPS <= int(O_COL), "S buffers overlap O");
+// tensor memory: S buffers 0..2 (KPS columns each; stage g uses g % 3 -- S_{g+3} waits for
+// PV_g, the buffer's reader), the Q tile (bf16 pairs: D / 2 columns, the A operand of
+// S = Q K^T, so the S MMAs read only K from shared memory), O_0, O_1
+constexpr int NSB = 3;
+constexpr uint32_t TMEM_COLS = 512, S_COL = 0, Q_COL = NSB * KPS, O_COL = 256;
+static_assert(Q_COL + D / 2 <= O_COL, "S buffers + Q overlap O");
 static_assert(SMEM <= 232448, "extend kernel shared memory");
 }  // namespace ext
 
@@ -128,9 +157,13 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
 #endif
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < NS; ++i) {
-            mbar_init(bar(BAR_FULL + i), 1);
-            mbar_init(bar(BAR_EMPTY + i), 1);
+        for (int i = 0; i < NK; ++i) {
+            mbar_init(bar(BAR_KFULL + i), KW);   // one expect-tx arrival per K producer warp
+            mbar_init(bar(BAR_KEMPTY + i), 1);
+        }
+        for (int i = 0; i < NV; ++i) {
+            mbar_init(bar(BAR_VFULL + i), 1);
+            mbar_init(bar(BAR_VEMPTY + i), 1);
         }
         for (int b = 0; b < 4; ++b) {
             mbar_init(bar(BAR_SFULL + b), 1);
@@ -139,6 +172,7 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
         }
         mbar_init(bar(BAR_QREADY), 256);
         mbar_init(bar(BAR_OFULL), 1);
+        for (int i = 0; i < QN; ++i) reinterpret_cast<int*>(smem + OFF_TSEQ)[i] = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) umma::tmem_alloc(sbase + OFF_TSLOT, TMEM_COLS);
@@ -148,8 +182,8 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
     const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + OFF_TSLOT);
     asm volatile("griddepcontrol.launch_dependents;");
     // stage timeline of CTA 0 (spa_debug_set_trace): lane 0 of warps 0..2 records (tag, clock64)
-    unsigned long long* trace = (p.trace && blockIdx.x == 0 && warp <= 2 && lane == 0)
-                                    ? p.trace + 2ull * warp * p.trace_cap : nullptr;
+    unsigned long long* trace = (p.trace && blockIdx.x == 0 && (warp <= 2 || warp == WARP_PV) && lane == 0)
+                                    ? p.trace + 2ull * (warp == WARP_PV ? 3 : warp) * p.trace_cap : nullptr;
     int tr_n = 0;
     auto tr = [&](unsigned long long tag, int id) {
         if (trace && tr_n < p.trace_cap) {
@@ -173,13 +207,17 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
     const int G = p.group_size, Hq = p.num_q_heads, Hkv = p.num_kv_heads;
     (void)Hq;
 
+    // A producer thread's TMA issue is slow and bounded by what it has in flight (measured,
+    // scripts/micro/tma_rate.cu: one issuing lane streams ~1-2 TB/s chip-wide, four lanes
+    // ~2.7-3.4, two warps x 4-8 lanes 5.3-7 TB/s): K and V are issued by separate warps, one
+    // box per lane.
+    uint64_t policy = 0;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+    volatile int* tseq = reinterpret_cast<volatile int*>(smem + OFF_TSEQ);
     if (warp == 0) {
-        // ------------------------------------------------------------ producer
-        uint64_t policy = 0;
-        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+        // ------------------------------------------------------------ K producer (leader): pops items
         bool waited = false;
-        int slot = 0, n = 0;
-        uint32_t ph = 0;
+        int n = 0, g = 0;   // g: global stage counter (K slot g % NK)
         for (int k = 0;; ++k) {
             int qi = 0;
             if (lane == 0) {
@@ -191,21 +229,27 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
             qi = __shfl_sync(0xffffffffu, qi, 0);
             const int it = qi < n_items ? queue[qi] : -1;
             ExtItem* e = &tq[n % QN];
-            ++n;
-            // the ring slot for this item's first stage (or the end marker)
-            EXT_WAIT(bar(BAR_EMPTY + slot), ph ^ 1u, 1);
+            // the K slot of this item's first stage (or the end marker): its fill publishes the
+            // entry to the MMA warp and the softmax WGs; tseq publishes it to the followers
+            EXT_WAIT(bar(BAR_KEMPTY + g % NK), uint32_t(((g / NK) & 1) ^ 1), 1);
             if (it < 0) {
                 if (lane == 0) {
                     e->it = -1;
-                    mbar_arrive(bar(BAR_FULL + slot));
+                    __threadfence_block();
+                    tseq[n % QN] = n + 1;
+                    mbar_arrive(bar(BAR_KFULL + g % NK));
                 }
                 break;
             }
             const Item itm = items[it];
             const Desc dsc = descs[itm.desc];
-            if (lane == 0)
+            if (lane == 0) {
                 *e = ExtItem{it, itm.kv_head, dsc.n_pages, dsc.tok_start, dsc.tok_end, dsc.member_off, dsc.n_members,
-                             dsc.kind};
+                             dsc.kind, dsc.page_off};
+                __threadfence_block();
+                tseq[n % QN] = n + 1;
+            }
+            ++n;
             if ((dsc.kind & 4) && !waited) {   // holds newest tokens: wait for their producer
                 asm volatile("griddepcontrol.wait;" ::: "memory");
                 waited = true;
@@ -213,154 +257,199 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
             int pid_cur = lane < dsc.n_pages ? pages[dsc.page_off + lane] : 0;
             int pid_base = 0;
             const int nst = (dsc.n_pages + PPS - 1) / PPS;
-            for (int st = 0; st < nst; ++st) {
-                if (st > 0) EXT_WAIT(bar(BAR_EMPTY + slot), ph ^ 1u, 2);
+            for (int st = 0; st < nst; ++st, ++g) {
+                const int ks = g % NK;
+                if (st > 0) EXT_WAIT(bar(BAR_KEMPTY + ks), uint32_t(((g / NK) & 1) ^ 1), 2);
                 tr(10, st);
                 const int p0 = st * PPS, npg = min(PPS, dsc.n_pages - p0);
-                int row[PPS];
-#pragma unroll
-                for (int j = 0; j < PPS; ++j) {
-                    const int kk = p0 + j;
-                    if (kk >= pid_base + 32) {
-                        pid_base += 32;
-                        pid_cur = pid_base + lane < dsc.n_pages ? pages[dsc.page_off + pid_base + lane] : 0;
-                    }
-                    const int page = __shfl_sync(0xffffffffu, pid_cur, (kk - pid_base) & 31);
-                    row[j] = p.layer_row_base + (page * Hkv + itm.kv_head) * kPageSize;
+                if (p0 >= pid_base + 32) {   // PPS divides 32: a stage never straddles a window
+                    pid_base += 32;
+                    pid_cur = pid_base + lane < dsc.n_pages ? pages[dsc.page_off + pid_base + lane] : 0;
                 }
-                if (lane == 0) {
-                    const uint32_t fb = bar(BAR_FULL + slot);
-                    mbar_expect_tx(fb, npg * 2 * PAGE_BYTES);
-                    const uint32_t sb = sbase + slot * STAGE_BYTES;
-                    for (int j = 0; j < npg; ++j) {
-                        tma_load_3d(sb + j * 2048, &tmk1, 0, row[j], 0, fb, policy);
-                        tma_load_3d(sb + K_CHUNK + j * 2048, &tmk1, 0, row[j], 1, fb, policy);
-                        tma_load_3d(sb + OFF_V + j * PAGE_BYTES, &tmv, 0, row[j], 0, fb, policy);
-                    }
-                }
+                // KW = 2: lane j < npg loads chunk 0 of page p0 + j; KW = 1: lane x < 2 npg loads
+                // chunk x % 2 of page p0 + x / 2
+                const int pj = KW == 2 ? lane : lane >> 1, ch = KW == 2 ? 0 : lane & 1;
+                const int page = __shfl_sync(0xffffffffu, pid_cur, (p0 - pid_base + pj) & 31);
+                const int row = p.layer_row_base + (page * Hkv + itm.kv_head) * kPageSize;
+                const uint32_t fb = bar(BAR_KFULL + ks);
+                if (lane == 0) mbar_expect_tx(fb, npg * PAGE_BYTES / KW);
                 __syncwarp();
+                if (lane < npg * (3 - KW))
+                    tma_load_3d(sbase + ks * HALF_BYTES + ch * K_CHUNK + pj * 2048, &tmk1, 0, row, ch, fb, policy);
+                __syncwarp();
+                tr(12, st);
                 if (lane == 0) {
                     EXT_DBG(0, n);
-                    EXT_DBG(1, slot);
+                    EXT_DBG(1, g);
                     EXT_DBG(2, st);
                     EXT_DBG(3, nst);
                 }
-                if (++slot == NS) {
-                    slot = 0;
-                    ph ^= 1u;
+            }
+        }
+    } else if (warp == WARP_V || warp == WARP_K1) {
+        // ------------------------------------------------------------ followers: the V producer and (KW = 2) the
+        // chunk-1 K producer walk the leader's items (published through tseq) and issue one
+        // box per lane and page into their ring
+        const bool is_v = warp == WARP_V;
+        const int nring = is_v ? NV : NK;
+        const uint32_t full0 = bar(is_v ? BAR_VFULL : BAR_KFULL), empty0 = bar(is_v ? BAR_VEMPTY : BAR_KEMPTY);
+        const uint32_t ring0 = sbase + (is_v ? OFF_V : K_CHUNK);   // K1: chunk 1 of each K stage
+        const CUtensorMap* tm = is_v ? &tmv : &tmk1;
+        const uint32_t box_bytes = is_v ? PAGE_BYTES : PAGE_BYTES / 2, box_stride = is_v ? PAGE_BYTES : 2048;
+        bool waited = false;
+        int n = 0, g = 0;   // g: global stage counter (slot g % nring)
+        while (true) {
+            if (lane == 0)
+                while (tseq[n % QN] != n + 1) __nanosleep(32);
+            __syncwarp();
+            __threadfence_block();
+            const ExtItem e = tq[n % QN];
+            ++n;
+            if (e.it < 0) {
+                if (!is_v) {   // the end marker's K slot also counts this warp's arrival
+                    EXT_WAIT(empty0 + (g % nring) * 8, uint32_t(((g / nring) & 1) ^ 1), 13);
+                    if (lane == 0) mbar_arrive(full0 + (g % nring) * 8);
                 }
+                break;
+            }
+            if ((e.kind & 4) && !waited) {
+                asm volatile("griddepcontrol.wait;" ::: "memory");
+                waited = true;
+            }
+            int pid_cur = lane < e.n_pages ? pages[e.page_off + lane] : 0;
+            int pid_base = 0;
+            const int nst = (e.n_pages + PPS - 1) / PPS;
+            for (int st = 0; st < nst; ++st, ++g) {
+                const int sl = g % nring;
+                EXT_WAIT(empty0 + sl * 8, uint32_t(((g / nring) & 1) ^ 1), 11);
+                const int p0 = st * PPS, npg = min(PPS, e.n_pages - p0);
+                if (p0 >= pid_base + 32) {
+                    pid_base += 32;
+                    pid_cur = pid_base + lane < e.n_pages ? pages[e.page_off + pid_base + lane] : 0;
+                }
+                const int page = __shfl_sync(0xffffffffu, pid_cur, (p0 - pid_base + lane) & 31);
+                const int row = p.layer_row_base + (page * Hkv + e.kv_head) * kPageSize;
+                const uint32_t fb = full0 + sl * 8;
+                if (lane == 0) mbar_expect_tx(fb, npg * box_bytes);
+                __syncwarp();
+                if (lane < npg)
+                    tma_load_3d(ring0 + sl * HALF_BYTES + lane * box_stride, tm, 0, row, is_v ? 0 : 1, fb, policy);
+                __syncwarp();
             }
         }
     } else if (warp == 1) {
-        // ------------------------------------------------------------ MMA issuer
-        // The whole warp walks the pipeline (its values stay warp-uniform, so descriptors
-        // live in uniform registers); one elected lane issues each batch of MMAs + commits.
-        const uint32_t id_o = umma::idesc_bf16_f32(128, 128, false, true);
-        const uint64_t q_desc = umma::desc_k_sw128(sbase + OFF_Q, 1024);
-        int slot = 0, n = 0;
-        uint32_t ph = 0, qph = 0;
-        uint32_t pph[4] = {0, 0, 0, 0};
-        int g = 0;   // running stage counter (S buffer = g & 1)
-        bool o_written[2] = {false, false};   // O_k has received a PV in this item
-        // PV of a stage is issued LAG stages after its S (S_g is queued before P_{g-2} is
-        // awaited), so each softmax warpgroup finds its next S ready when it finishes one
-        constexpr int LAG = 2;
-        int lag_slot[LAG + 1] = {}, lag_npg[LAG + 1] = {}, lag_g[LAG + 1] = {};   // pending stages (one pushed before a retire)
-        int n_lag = 0;
-        auto retire = [&]() {   // wait for the oldest pending stage's P, then O_b += P V
-            const int gg = lag_g[0], b = gg & 1, ps = lag_slot[0], pn = lag_npg[0];
-            EXT_WAIT(bar(BAR_PFULL + (gg & 3)), pph[gg & 3], 7);
-            pph[gg & 3] ^= 1u;
-            umma::fence_after();
-            const uint64_t v_desc = umma::desc_mn_sw128(sbase + ps * STAGE_BYTES + OFF_V, 2048, 1024);
-            if (umma::elect_one()) {
-                for (int pg = 0; pg < pn; ++pg)
-                    umma::mma_ts(tmem + O_COL + b * 128, tmem + S_COL + (gg & 3) * KPS + pg * 8,
-                                 v_desc + uint64_t((pg * PAGE_BYTES) >> 4), id_o, o_written[b] || pg > 0);
-                umma::commit(bar(BAR_EMPTY + ps));
-                umma::commit(bar(BAR_PVDONE + (gg & 3)));
-            }
-            __syncwarp();
-            o_written[b] = true;
-            for (int i = 0; i + 1 < n_lag; ++i) {
-                lag_slot[i] = lag_slot[i + 1];
-                lag_npg[i] = lag_npg[i + 1];
-                lag_g[i] = lag_g[i + 1];
-            }
-            --n_lag;
-        };
+        // ------------------------------------------------------------ S issuer
+        // S_g = Q K_g^T into S buffer g % 3 once K_g landed and PV_{g-3} (the buffer's last
+        // reader) completed.  S and PV are issued by different warps: one thread's tcgen05.mma
+        // issue blocks while the tensor pipe works, so one issuer serialises S and PV.  The
+        // whole warp walks the pipeline (descriptors stay warp-uniform); one lane issues.
+        int n = 0, g = 0;   // g: global stage counter (K slot g % NK, S buffer g % 3)
+        uint32_t qph = 0;
         while (true) {
-            EXT_WAIT(bar(BAR_FULL + slot), ph, 3);
+            EXT_WAIT(bar(BAR_KFULL + g % NK), uint32_t((g / NK) & 1), 3);
             const ExtItem e = tq[n % QN];
             ++n;
             if (e.it < 0) break;
+            tr(22, n);
             EXT_WAIT(bar(BAR_QREADY), qph, 4);   // Q tile written (and the last item's O read out)
             qph ^= 1u;
-            umma::fence_after();
-            o_written[0] = o_written[1] = false;
+            tr(23, n);
             const int nst = (e.n_pages + PPS - 1) / PPS;
             for (int st = 0; st < nst; ++st, ++g) {
+                const int ks = g % NK;
                 if (lane == 0) {
                     EXT_DBG(4, n);
                     EXT_DBG(5, g);
                     EXT_DBG(6, st);
                     EXT_DBG(7, nst);
                 }
-                if (st > 0) EXT_WAIT(bar(BAR_FULL + slot), ph, 5);
+                if (st > 0) EXT_WAIT(bar(BAR_KFULL + ks), uint32_t((g / NK) & 1), 5);
+                // S buffer g % 3 is free once PV_{g-3} completed (its completion (g-3)/3; the next
+                // one needs S_g, so the parity is exact)
+                if (g >= NSB) EXT_WAIT(bar(BAR_PVDONE + g % NSB), uint32_t(((g - NSB) / NSB) & 1), 14);
                 tr(20, st);
                 umma::fence_after();
                 const int npg = min(PPS, e.n_pages - st * PPS);
-                const uint64_t k_desc = umma::desc_k_sw128(sbase + slot * STAGE_BYTES, 1024);
-                const uint32_t sbuf = tmem + S_COL + (g & 3) * KPS;
+                const uint64_t k_desc = umma::desc_k_sw128(sbase + ks * HALF_BYTES, 1024);
+                const uint32_t sbuf = tmem + S_COL + (g % NSB) * KPS;
                 const uint32_t id_s = umma::idesc_bf16_f32(128, npg * 16, false, false);
                 if (umma::elect_one()) {
 #pragma unroll
-                    for (int ks = 0; ks < D / 16; ++ks)   // 16-B units: chunk stride, 32 B per K step
-                        umma::mma_ss(sbuf, q_desc + uint64_t((ks >> 2) * (16384 >> 4) + (ks & 3) * 2),
-                                     k_desc + uint64_t((ks >> 2) * (K_CHUNK >> 4) + (ks & 3) * 2), id_s, ks > 0);
-                    umma::commit(bar(BAR_SFULL + (g & 3)));
+                    for (int kk = 0; kk < D / 16 && !(EXP & 1); ++kk)   // A: Q columns (8 per K step); B: 16-B units
+                        umma::mma_ts(sbuf, tmem + Q_COL + kk * 8,
+                                     k_desc + uint64_t((kk >> 2) * (K_CHUNK >> 4) + (kk & 3) * 2), id_s, kk > 0);
+                    umma::commit(bar(BAR_KEMPTY + ks));   // K slot free once S_g has read it
+                    umma::commit(bar(BAR_SFULL + g % NSB));
                 }
                 __syncwarp();
                 tr(21, st);
-                lag_slot[n_lag] = slot;
-                lag_npg[n_lag] = npg;
-                lag_g[n_lag] = g;
-                ++n_lag;
-                if (n_lag > LAG) retire();
-                if (++slot == NS) {
-                    slot = 0;
-                    ph ^= 1u;
-                }
             }
-            while (n_lag > 0) retire();   // the item's last PVs, then O is complete
-            if (umma::elect_one()) umma::commit(bar(BAR_OFULL));
+        }
+    } else if (warp == WARP_PV) {
+        // ------------------------------------------------------------ PV issuer
+        // O_{g & 1} += P_g V_g once the softmax WG wrote P_g and V_g landed; after an item's
+        // last PV, o_full.  Follows the K producer's items through tseq.
+        const uint32_t id_o = umma::idesc_bf16_f32(128, 128, false, true);
+        int n = 0, g = 0;
+        while (true) {
+            if (lane == 0)
+                while (tseq[n % QN] != n + 1) __nanosleep(32);
+            __syncwarp();
+            __threadfence_block();
+            const ExtItem e = tq[n % QN];
+            ++n;
+            if (e.it < 0) break;
+            bool o_written[2] = {false, false};   // O_k has received a PV in this item
+            const int nst = (e.n_pages + PPS - 1) / PPS;
+            for (int st = 0; st < nst; ++st, ++g) {
+                const int b = g & 1, vs = g % NV, pn = min(PPS, e.n_pages - st * PPS);
+                EXT_WAIT(bar(BAR_PFULL + g % NSB), uint32_t((g / NSB) & 1), 7);
+                tr(24, g);
+                EXT_WAIT(bar(BAR_VFULL + vs), uint32_t((g / NV) & 1), 12);
+                tr(25, g);
+                umma::fence_after();
+                const uint64_t v_desc = umma::desc_mn_sw128(sbase + OFF_V + vs * HALF_BYTES, 2048, 1024);
+                if (umma::elect_one()) {
+                    for (int pg = 0; pg < pn && !(EXP & 1); ++pg)
+                        umma::mma_ts(tmem + O_COL + b * 128, tmem + S_COL + (g % NSB) * KPS + pg * 8,
+                                     v_desc + uint64_t((pg * PAGE_BYTES) >> 4), id_o, o_written[b] || pg > 0);
+                    umma::commit(bar(BAR_VEMPTY + vs));
+                    umma::commit(bar(BAR_PVDONE + g % NSB));
+                }
+                __syncwarp();
+                tr(26, g);
+                o_written[b] = true;
+            }
+            if (umma::elect_one()) umma::commit(bar(BAR_OFULL));   // the item's O is complete
             __syncwarp();
         }
     } else {
         // ------------------------------------------------------------ softmax warpgroups
         // WG k (warps 2 + 4k .. 5 + 4k) takes the stages of parity k (global stage counter)
         // with its own running (m, l) and its own O accumulator O_k; PV of stage g adds into
-        // O_{g & 1}, so a WG's O is stable whenever its S_g has landed (S_g was issued after
-        // PV_{g-2}) and rescaling needs no extra wait.  At item end the two halves merge.
+        // O_{g & 1}.  Rescaling O_k waits for the WG's previous PV (pv_done); the next PV into
+        // O_k needs this stage's P, so nothing else writes O_k meanwhile.  At item end the two
+        // halves merge.
         const int wgk = (warp - 2) >> 2;
         const int row = 32 * (warp & 3) + lane;          // query row = tensor-memory lane
         const uint32_t lane_off = uint32_t(32 * (warp & 3)) << 16;
         const uint32_t o_mine = tmem + lane_off + O_COL + wgk * 128;
         float* ml = reinterpret_cast<float*>(smem + OFF_ML);   // [2 WGs][2][128]: m, l per row
         asm volatile("griddepcontrol.wait;" ::: "memory");   // q and the outputs belong to the stream
-        int n = 0, g = 0;   // g: global stage counter (ring slot g % NS, phase (g / NS) & 1)
-        uint32_t oph = 0, sph[2] = {0, 0};   // phases of this WG's S buffers k, k + 2
+        int n = 0, g = 0;   // g: global stage counter (K slot g % NK, phase (g / NK) & 1)
+        uint32_t oph = 0;
         constexpr float kRescale = 8.f;
         auto wg_sync = [&]() { asm volatile("bar.sync 1, 256;" ::: "memory"); };
         while (true) {
-            // the item's first stage landed: its entry is valid.  Only the first stage's
-            // slot is awaited here (its next fill needs this item's P, so it cannot run
-            // ahead); the other stages are tracked through s_full.
-            EXT_WAIT(bar(BAR_FULL + g % NS), uint32_t((g / NS) & 1), 8);
+            // the item's first K stage landed: its entry is valid.  Only that slot is awaited
+            // here; the other stages are tracked through s_full.  The slot cannot complete
+            // its next fill first: that needs S_g, which waits for this item's Q tile.
+            EXT_WAIT(bar(BAR_KFULL + g % NK), uint32_t((g / NK) & 1), 8);
             const ExtItem e = tq[n % QN];
             ++n;
             if (e.it < 0) break;
             const int R = e.n_members * G;
+            tr(32, n);
             // ---- row setup + this WG's half of the Q tile (K-major SW128: 64-column chunk
             //      c = wgk of row r at c * 16 KB + sw128(r, u))
             int lo = 0, hi = 0, mrow = 0, rec = -1, head = 0;
@@ -381,11 +470,13 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
 #pragma unroll
                 for (int u = 0; u < 8; ++u) qv[u] = make_uint4(0u, 0u, 0u, 0u);
             }
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-                *reinterpret_cast<uint4*>(smem + OFF_Q + wgk * 16384 + umma::sw128_offset(row, u)) = qv[u];
-            umma::fence_proxy_async_smem();
+            // this WG's half of the Q row (channels [64 k, 64 k + 64)) into tensor-memory
+            // columns Q_COL + 32 k .. (bf16 pairs, lane = row: the A operand layout of S)
+            umma::st32(tmem + lane_off + Q_COL + wgk * 32, reinterpret_cast<const float*>(qv));
+            umma::wait_st();
+            umma::fence_before();
             mbar_arrive(bar(BAR_QREADY));
+            tr(33, n);
 
             float m_run = -INFINITY, l_run = 0.f;
             bool mine_any = false;   // did this WG take a stage of the item (O_k written)?
@@ -396,14 +487,19 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
                     EXT_DBG(9, n);
                 }
                 if ((g & 1) == wgk) {
-                    EXT_WAIT(bar(BAR_SFULL + (g & 3)), sph[(g >> 1) & 1], 9);
-                    sph[(g >> 1) & 1] ^= 1u;
+                    EXT_WAIT(bar(BAR_SFULL + g % NSB), uint32_t((g / NSB) & 1), 9);
                     tr(30, st);
+                    if (EXP & 2) {
+                        umma::fence_before();
+                        mbar_arrive(bar(BAR_PFULL + g % NSB));
+                        mine_any = true;
+                        continue;
+                    }
                     umma::fence_after();
                     float s[KPS];
 #pragma unroll
                     for (int c = 0; c < KPS / 32; ++c)
-                        umma::ld32(tmem + lane_off + S_COL + (g & 3) * KPS + c * 32, s + c * 32);
+                        umma::ld32(tmem + lane_off + S_COL + (g % NSB) * KPS + c * 32, s + c * 32);
                     umma::wait_ld();
                     const int npg = min(PPS, e.n_pages - st * PPS);
                     const int tok0 = e.tok_start + st * KPS;
@@ -430,11 +526,10 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
                         l_run *= al;
                         m_run = mn;
                         if (mine_any) {   // O_k holds this WG's earlier stages
-                            // PV of this WG's previous stage g - 2 may still run (PV lags S by
-                            // LAG = 2): wait for it.  pv_done[(g-2) % 4] completes once per 4
-                            // stages; PV g-6 is complete (issued before S g) and PV g+2 needs
-                            // P g, so the parity of completion (g-2) / 4 is exact.
-                            EXT_WAIT(bar(BAR_PVDONE + ((g - 2) & 3)), uint32_t(((g - 2) >> 2) & 1), 10);
+                            // PV of this WG's previous stage g - 2 may still run: wait for it.  pv_done[(g-2) % 3] completes once per 3
+                            // stages; PV g+1 (same buffer) needs P g, so it cannot have
+                            // completed yet and the parity of completion (g-2) / 3 is exact.
+                            EXT_WAIT(bar(BAR_PVDONE + (g - 2) % NSB), uint32_t(((g - 2) / NSB) & 1), 10);
                             umma::fence_after();
 #pragma unroll 1
                             for (int c = 0; c < 4; ++c) {
@@ -461,17 +556,19 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
                     l_run += (lp[0] + lp[1]) + (lp[2] + lp[3]);
 #pragma unroll
                     for (int c = 0; c < KPS / 32; ++c)
-                        umma::st16(tmem + lane_off + S_COL + (g & 3) * KPS + c * 16, pk + c * 16);
+                        umma::st16(tmem + lane_off + S_COL + (g % NSB) * KPS + c * 16, pk + c * 16);
                     umma::wait_st();
                     umma::fence_before();
-                    mbar_arrive(bar(BAR_PFULL + (g & 3)));
+                    mbar_arrive(bar(BAR_PFULL + g % NSB));
                     tr(31, st);
                     mine_any = true;
                 }
             }
             // ---- epilogue: both O halves complete; merge the two WGs' softmax states per row
+            tr(34, n);
             EXT_WAIT(bar(BAR_OFULL), oph, 6);
             oph ^= 1u;
+            tr(35, n);
             umma::fence_after();
             ml[(wgk * 2 + 0) * 128 + row] = m_run;
             ml[(wgk * 2 + 1) * 128 + row] = l_run;
@@ -529,6 +626,7 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
             }
             umma::fence_before();
             wg_sync();   // ml is rewritten at the next item's end; O is free for the next item
+            tr(36, n);
         }
     }
 
