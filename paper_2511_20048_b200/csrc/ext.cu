@@ -121,17 +121,22 @@ constexpr int OFF_BAR = (NK + NV) * HALF_BYTES;
 // using S buffer b)
 constexpr int BAR_KFULL = 0, BAR_KEMPTY = NK, BAR_VFULL = 2 * NK, BAR_VEMPTY = 2 * NK + NV,
               BAR_SFULL = 2 * (NK + NV), BAR_PFULL = BAR_SFULL + 4, BAR_QREADY = BAR_SFULL + 8,
-              BAR_OFULL = BAR_SFULL + 9, BAR_PVDONE = BAR_SFULL + 10, N_BARS = BAR_SFULL + 14;
+              BAR_OFULL = BAR_SFULL + 9, BAR_PVDONE = BAR_SFULL + 10, BAR_OFREE = BAR_SFULL + 14,
+              N_BARS = BAR_SFULL + 15;
 constexpr int OFF_TQ = OFF_BAR + N_BARS * 8;
 constexpr int OFF_TSEQ = OFF_TQ + QN * int(sizeof(ExtItem));   // int[QN]: entry n published as n + 1
 constexpr int OFF_ML = (OFF_TSEQ + QN * 4 + 15) & ~15;           // [2][2][128] fp32 + 8 flags
 constexpr int OFF_TSLOT = OFF_ML + 4 * 128 * 4 + 8 * 4;
 constexpr int SMEM = 1024 + OFF_TSLOT + 16 + 128;   // + debug words (hang-trap builds)
-constexpr int KW = 2;   // K producer warps (one 64-channel chunk each)
-// warps: 0 K producer (chunk 0, pops items), 1 S issuer, 2-9 softmax warpgroups, 10 V producer,
-// 11 K producer (chunk 1), 12 PV issuer
-constexpr int THREADS = 13 * 32;
-constexpr int WARP_V = 10, WARP_K1 = 11, WARP_PV = 12;
+#ifndef SPA_EXT_KW
+#define SPA_EXT_KW 1
+#endif
+constexpr int KW = SPA_EXT_KW;   // K producer warps: 1, or 2 (one 64-channel chunk each; warp 12)
+static_assert(KW == 1 || KW == 2, "K producer warps");
+// warps: 0 K producer (pops items), 1 S issuer, 2-9 softmax warpgroups, 10 V producer, 11 PV issuer,
+// 12 (KW = 2) K producer of chunk 1
+constexpr int THREADS = (11 + KW) * 32;
+constexpr int WARP_V = 10, WARP_PV = 11, WARP_K1 = 12;
 // tensor memory: S buffers 0..3 (KPS columns each; stage g uses g % 4), O_0, O_1 (128 each)
 // tensor memory: S buffers 0..2 (KPS columns each; stage g uses g % 3 -- S_{g+3} waits for
 // PV_g, the buffer's reader), the Q tile (bf16 pairs: D / 2 columns, the A operand of
@@ -172,6 +177,7 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
         }
         mbar_init(bar(BAR_QREADY), 256);
         mbar_init(bar(BAR_OFULL), 1);
+        mbar_init(bar(BAR_OFREE), 256);
         for (int i = 0; i < QN; ++i) reinterpret_cast<int*>(smem + OFF_TSEQ)[i] = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -399,6 +405,10 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
             const ExtItem e = tq[n % QN];
             ++n;
             if (e.it < 0) break;
+            if (n > 1) {   // the previous item's epilogue has read O_0 / O_1 (completion n - 2)
+                EXT_WAIT(bar(BAR_OFREE), uint32_t((n - 2) & 1), 15);
+                umma::fence_after();
+            }
             bool o_written[2] = {false, false};   // O_k has received a PV in this item
             const int nst = (e.n_pages + PPS - 1) / PPS;
             for (int st = 0; st < nst; ++st, ++g) {
@@ -436,48 +446,67 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
         const uint32_t o_mine = tmem + lane_off + O_COL + wgk * 128;
         float* ml = reinterpret_cast<float*>(smem + OFF_ML);   // [2 WGs][2][128]: m, l per row
         asm volatile("griddepcontrol.wait;" ::: "memory");   // q and the outputs belong to the stream
-        int n = 0, g = 0;   // g: global stage counter (K slot g % NK, phase (g / NK) & 1)
+        int g = 0;   // g: global stage counter (S buffer g % 3)
         uint32_t oph = 0;
         constexpr float kRescale = 8.f;
         auto wg_sync = [&]() { asm volatile("bar.sync 1, 256;" ::: "memory"); };
-        while (true) {
-            // the item's first K stage landed: its entry is valid.  Only that slot is awaited
-            // here; the other stages are tracked through s_full.  The slot cannot complete
-            // its next fill first: that needs S_g, which waits for this item's Q tile.
-            EXT_WAIT(bar(BAR_KFULL + g % NK), uint32_t((g / NK) & 1), 8);
-            const ExtItem e = tq[n % QN];
-            ++n;
-            if (e.it < 0) break;
-            const int R = e.n_members * G;
-            tr(32, n);
-            // ---- row setup + this WG's half of the Q tile (K-major SW128: 64-column chunk
-            //      c = wgk of row r at c * 16 KB + sw128(r, u))
-            int lo = 0, hi = 0, mrow = 0, rec = -1, head = 0;
-            const bool live = row < R;
-            uint4 qv[8];
-            if (live) {
+        // Items are read ahead through tseq: at the end of item n the next item's member rows
+        // and Q half-rows are loaded while the last PVs run, written into tensor memory right
+        // after o_full (every S of item n has completed by then), and q_ready lets the S issuer
+        // start item n + 1 while this WG's epilogue reads O; the PV issuer waits for o_free.
+        struct Rows {
+            int lo, hi, mrow, rec, head;
+            bool live;
+        };
+        auto read_entry = [&](int idx) {
+            if (lane == 0)
+                while (tseq[idx % QN] != idx + 1) __nanosleep(32);
+            __syncwarp();
+            __threadfence_block();
+            return tq[idx % QN];
+        };
+        auto load_rows = [&](const ExtItem& e, Rows& r, uint4* qv) {
+            // padding rows attend to everything (their S is 0: Q is zero) so that their warp
+            // keeps the unmasked fast path; their results are never stored
+            r = Rows{0, 0x7fffffff, 0, -1, 0, e.it >= 0 && row < e.n_members * G};
+            if (r.live) {
                 const int mb = row / G;
                 const Member m = mems[e.member_off + mb];
-                lo = m.lo;
-                hi = m.hi;
-                mrow = m.row;
-                rec = m.rec;
-                head = e.kv_head * G + (row - mb * G);
-                const uint4* src = reinterpret_cast<const uint4*>(p.q + m.row * p.q_sr + head * p.q_sh) + wgk * 8;
+                r.lo = m.lo;
+                r.hi = m.hi;
+                r.mrow = m.row;
+                r.rec = m.rec;
+                r.head = e.kv_head * G + (row - mb * G);
+                const uint4* src = reinterpret_cast<const uint4*>(p.q + m.row * p.q_sr + r.head * p.q_sh) + wgk * 8;
 #pragma unroll
                 for (int u = 0; u < 8; ++u) qv[u] = src[u];
             } else {
 #pragma unroll
                 for (int u = 0; u < 8; ++u) qv[u] = make_uint4(0u, 0u, 0u, 0u);
             }
-            // this WG's half of the Q row (channels [64 k, 64 k + 64)) into tensor-memory
-            // columns Q_COL + 32 k .. (bf16 pairs, lane = row: the A operand layout of S)
+        };
+        // this WG's half of the Q rows (channels [64 k, 64 k + 64)) into tensor-memory columns
+        // Q_COL + 32 k .. (bf16 pairs, lane = row: the A operand layout of S), then q_ready
+        auto put_q = [&](const uint4* qv) {
             umma::st32(tmem + lane_off + Q_COL + wgk * 32, reinterpret_cast<const float*>(qv));
             umma::wait_st();
             umma::fence_before();
             mbar_arrive(bar(BAR_QREADY));
-            tr(33, n);
-
+        };
+        ExtItem e = read_entry(0);
+        int n = 1;
+        Rows rw;
+        {
+            uint4 qv[8];
+            load_rows(e, rw, qv);
+            if (e.it >= 0) put_q(qv);
+        }
+        while (e.it >= 0) {
+            tr(32, n);
+            const int lo = rw.lo, hi = rw.hi;
+            // a warp whose 32 rows are all padding (R <= 96 of the 128-row tile) skips its tensor-
+            // memory traffic: its P / O lanes hold stale values that only feed padding rows
+            const bool wdead = 32 * (warp & 3) >= e.n_members * G;
             float m_run = -INFINITY, l_run = 0.f;
             bool mine_any = false;   // did this WG take a stage of the item (O_k written)?
             const int nst = (e.n_pages + PPS - 1) / PPS;
@@ -489,7 +518,7 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
                 if ((g & 1) == wgk) {
                     EXT_WAIT(bar(BAR_SFULL + g % NSB), uint32_t((g / NSB) & 1), 9);
                     tr(30, st);
-                    if (EXP & 2) {
+                    if ((EXP & 2) || wdead) {
                         umma::fence_before();
                         mbar_arrive(bar(BAR_PFULL + g % NSB));
                         mine_any = true;
@@ -501,6 +530,13 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
                     for (int c = 0; c < KPS / 32; ++c)
                         umma::ld32(tmem + lane_off + S_COL + (g % NSB) * KPS + c * 32, s + c * 32);
                     umma::wait_ld();
+                    if (trace) {   // make the S-loaded stamp wait for the load's registers
+                        float d0, d1;
+                        asm volatile("mov.b32 %0, %1;" : "=f"(d0) : "f"(s[0]));
+                        asm volatile("mov.b32 %0, %1;" : "=f"(d1) : "f"(s[KPS - 1]));
+                        if (d0 == 1.2345f && d1 == 5.4321f) tr(42, st);
+                    }
+                    tr(37, st);
                     const int npg = min(PPS, e.n_pages - st * PPS);
                     const int tok0 = e.tok_start + st * KPS;
                     const int kmax = min(min(hi, e.tok_end), tok0 + npg * 16);   // keys [max(lo,tok0), kmax) live
@@ -517,6 +553,7 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
                         }
                     }
                     mx *= p.scale_log2;
+                    tr(41, st);
                     // lazy rescale (P <= 2^kRescale), decided per warp: tensor-memory loads and
                     // stores are warp-collective, so a warp rescales all its rows together
                     const bool grow = mx > m_run + kRescale || (m_run == -INFINITY && mx > -INFINITY);
@@ -541,8 +578,10 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
                                 umma::st32(o_mine + c * 32, ov);
                             }
                             umma::wait_st();
+                            tr(40, st);
                         }
                     }
+                    tr(38, st);
                     const float mu = m_run == -INFINITY ? 0.f : m_run;
                     uint32_t pk[KPS / 2];
                     float lp[4] = {0.f, 0.f, 0.f, 0.f};   // independent partial sums (short add chains)
@@ -554,6 +593,7 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
                         pk[i] = pack_bf16(e0, e1);
                     }
                     l_run += (lp[0] + lp[1]) + (lp[2] + lp[3]);
+                    tr(39, st);
 #pragma unroll
                     for (int c = 0; c < KPS / 32; ++c)
                         umma::st16(tmem + lane_off + S_COL + (g % NSB) * KPS + c * 16, pk + c * 16);
@@ -564,12 +604,21 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
                     mine_any = true;
                 }
             }
+            // ---- the next item: rows + Q loads in flight while the last PVs run
+            const ExtItem nx = read_entry(n);
+            ++n;
+            Rows rn;
+            uint4 qn[8];
+            load_rows(nx, rn, qn);
             // ---- epilogue: both O halves complete; merge the two WGs' softmax states per row
             tr(34, n);
             EXT_WAIT(bar(BAR_OFULL), oph, 6);
             oph ^= 1u;
             tr(35, n);
             umma::fence_after();
+            if (nx.it >= 0) put_q(qn);   // every S of this item completed before o_full
+            const bool live = rw.live;
+            const int mrow = rw.mrow, rec = rw.rec, head = rw.head;
             ml[(wgk * 2 + 0) * 128 + row] = m_run;
             ml[(wgk * 2 + 1) * 128 + row] = l_run;
             const uint32_t used = __ballot_sync(0xffffffffu, mine_any);   // uniform per WG
@@ -585,7 +634,7 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
             const float w0 = a0 * inv, w1 = a1 * inv;
             // WG k writes output columns [64 k, 64 k + 64)
 #pragma unroll 1
-            for (int c = 0; c < 2; ++c) {
+            for (int c = 0; c < 2 && !wdead; ++c) {
                 const int col = wgk * 64 + c * 32;
                 float o0[32], o1[32];
                 if (have0) {
@@ -625,8 +674,11 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
                 }
             }
             umma::fence_before();
-            wg_sync();   // ml is rewritten at the next item's end; O is free for the next item
+            mbar_arrive(bar(BAR_OFREE));   // O_0 / O_1 may take the next item's PVs
+            wg_sync();   // ml is rewritten at the next item's end
             tr(36, n);
+            e = nx;
+            rw = rn;
         }
     }
 

@@ -14,7 +14,7 @@ from paper_2511_20048_b200 import spa  # noqa: E402
 from spa_inputs import KIND_Q, kv_bits_torch, workloads  # noqa: E402
 
 NAMES = {10: "P issue", 11: "P rows", 12: "P K-issued", 13: "P V-free", 20: "M kfull", 21: "M S-issued", 22: "M item", 23: "M qready", 24: "M P-ready", 25: "M V-ready", 26: "M PV-issued", 30: "W sfull",
-         31: "W pfull-arr", 32: "W item", 33: "W q-written", 34: "W epi-wait", 35: "W ofull", 36: "W item-done"}
+         31: "W pfull-arr", 32: "W item", 33: "W q-written", 34: "W epi-wait", 35: "W ofull", 36: "W item-done", 37: "W S-loaded", 38: "W max-done", 39: "W exp-done", 40: "W O-rescaled", 41: "W max-only"}
 
 
 def main():
