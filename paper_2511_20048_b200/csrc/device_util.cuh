@@ -42,6 +42,17 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "memory");
 }
 
+// non-blocking: has the phase of parity `parity` completed?
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar,
                                             uint64_t policy) {
     asm volatile(
@@ -480,6 +491,64 @@ __device__ __forceinline__ void warp_merge_head(const float* part_o, const float
         }
     }
     if (lane == 0 && lrow) st_out1(fan, lrow + (long long)head * l_sh, lse);
+}
+
+// A whole (row, KV head) task with exactly S = 2 records (a shared range + a tail: the common
+// case of prefix sharing), G <= 8 heads: every lane loads both LSEs and its float4 column of
+// both partial rows of every head up front (one L2 round trip, no shuffles), then reduces in
+// registers.  Per head the arithmetic is warp_merge_head's S <= 16 path (max; butterfly sum
+// of exp(LSE_j - m), which for two live lanes is e_0 + e_1; weights exp(LSE_j - LSE); FMAs in
+// record order), so the result has the same bits.
+template <int DT>
+__device__ __forceinline__ void warp_merge_task_s2(const float* part_o, const float* part_lse, int H, int s0,
+                                                   int head0, int G, __nv_bfloat16* orow, long long o_sh,
+                                                   float* lrow, long long l_sh, int lane) {
+    constexpr int D = DT;
+    const int c = lane * 4;
+    float l0[8], l1[8];
+    float4 v0[8], v1[8];
+#pragma unroll
+    for (int hh = 0; hh < 8; ++hh) {
+        if (hh < G) {
+            l0[hh] = __ldcg(part_lse + (long long)s0 * H + head0 + hh);
+            l1[hh] = __ldcg(part_lse + (long long)(s0 + 1) * H + head0 + hh);
+            if (c < D) {
+                v0[hh] = __ldcg(reinterpret_cast<const float4*>(part_o + ((long long)s0 * H + head0 + hh) * D + c));
+                v1[hh] = __ldcg(reinterpret_cast<const float4*>(part_o + ((long long)(s0 + 1) * H + head0 + hh) * D + c));
+            }
+        }
+    }
+#pragma unroll
+    for (int hh = 0; hh < 8; ++hh) {
+        if (hh < G) {
+            const float m = fmaxf(l0[hh], l1[hh]);
+            const float e0 = (l0[hh] != -INFINITY) ? expf(l0[hh] - m) : 0.f;
+            const float e1 = (l1[hh] != -INFINITY) ? expf(l1[hh] - m) : 0.f;
+            const float e = e0 + e1;
+            const float lse = (m == -INFINITY) ? -INFINITY : m + logf(e);
+            const float w0 = (l0[hh] != -INFINITY) ? expf(l0[hh] - lse) : 0.f;
+            const float w1 = (l1[hh] != -INFINITY) ? expf(l1[hh] - lse) : 0.f;
+            float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (w0 != 0.f) {
+                a.x += w0 * v0[hh].x;
+                a.y += w0 * v0[hh].y;
+                a.z += w0 * v0[hh].z;
+                a.w += w0 * v0[hh].w;
+            }
+            if (w1 != 0.f) {
+                a.x += w1 * v1[hh].x;
+                a.y += w1 * v1[hh].y;
+                a.z += w1 * v1[hh].z;
+                a.w += w1 * v1[hh].w;
+            }
+            if (c < D) {
+                __nv_bfloat16* op = orow + (long long)(head0 + hh) * o_sh + c;
+                st_out2(nullptr, op, a.x, a.y);
+                st_out2(nullptr, op + 2, a.z, a.w);
+            }
+            if (lane == 0 && lrow) st_out1(nullptr, lrow + (long long)(head0 + hh) * l_sh, lse);
+        }
+    }
 }
 
 // Merge heads [head0, head0 + G) of one request row: all G in one warp pass when

@@ -187,6 +187,11 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
     umma::fence_after();
     const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + OFF_TSLOT);
     asm volatile("griddepcontrol.launch_dependents;");
+    if (p.trace && threadIdx.x == 0 && int(blockIdx.x) < p.trace_cap) {
+        unsigned long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        p.trace[2ull * (7ull * p.trace_cap + blockIdx.x)] = gt;
+    }
     // stage timeline of CTA 0 (spa_debug_set_trace): lane 0 of warps 0..2 records (tag, clock64)
     unsigned long long* trace = (p.trace && blockIdx.x == 0 && (warp <= 2 || warp == WARP_PV) && lane == 0)
                                     ? p.trace + 2ull * (warp == WARP_PV ? 3 : warp) * p.trace_cap : nullptr;
@@ -686,6 +691,11 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
     umma::fence_before();
     __syncthreads();
     umma::fence_after();
+    if (p.trace && threadIdx.x == 0 && int(blockIdx.x) < p.trace_cap) {   // per-CTA (start, end) in row 7
+        unsigned long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        p.trace[2ull * (7ull * p.trace_cap + blockIdx.x) + 1] = gt;
+    }
     if (warp == 1) umma::tmem_dealloc(tmem, TMEM_COLS);
     if (threadIdx.x == 0) {
         if (atomicAdd(sched + 1, 1) == int(gridDim.x) - 1) {
@@ -735,9 +745,10 @@ int launch_ext(const spa_plan* P, int32_t layer, const void* q, int64_t q_sr, in
     const CUtensorMap* tv = reinterpret_cast<const CUtensorMap*>(P->pool->tmap_v.bytes);
     int err = launch_pdl(ext_kernel, dim3(P->num_ctas), dim3(ext::THREADS), ext::SMEM, stream, *tk, *tv, ep);
     if (err) return err;
-    if (H[H_N_RECORDS] > 0)
-        err = launch_merge(H[H_N_REQ], c.num_q_heads, c.head_dim, P->d_meta + H[H_OFF_REC_PTR], P->d_part_o,
-                           P->d_part_lse, o, o_sr, o_sh, lse, l_sr, l_sh, P->num_ctas, stream);
+    // split partials: one warp per merge subtask of the plan in its own launch (programmatic
+    // dependent launch; an in-kernel tail merge measured slower: the merges wait for the last
+    // items, and its registers spill in the streaming loops)
+    if (H[H_N_RECORDS] > 0) err = launch_merge_tasks(P, o, o_sr, o_sh, lse, l_sr, l_sh, stream);
     return err;
 }
 

@@ -304,6 +304,58 @@ __global__ void __launch_bounds__(256, 1) merge_kernel(const MergeParams p) {
     }
 }
 
+// A plan's split merge as its own launch (the tcgen05 extend path): one warp per merge
+// subtask of the plan's list (a whole (row, KV head) task -- all G heads x S records loaded in
+// one L2 round trip -- or one head of it), the whole list in one wave.  The plan metadata is
+// read before the programmatic-dependency wait (it was uploaded earlier in stream order),
+// the partials after it.
+template <int D, bool S2>   // S2: every subtask is a whole task of exactly 2 records (lean registers)
+__global__ void __launch_bounds__(128) merge_tasks_kernel(const int32_t* meta, const MergeParams p, int G, int Hkv) {
+    const int lane = threadIdx.x & 31;
+    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int n_sub = meta[H_N_MTASK];
+    int code = 0, s0 = 0, s1 = 0;
+    if (t < n_sub) {
+        code = meta[meta[H_OFF_MTASK] + t];
+        const int row = (code >> 8) / Hkv;
+        s0 = p.rec_ptr[row];
+        s1 = p.rec_ptr[row + 1];
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // partials come from the attention kernel
+    asm volatile("griddepcontrol.launch_dependents;");
+    if (t >= n_sub) return;
+    const int task = code >> 8, sub = code & 255;
+    const int row = task / Hkv, kvh = task - row * Hkv;
+    __nv_bfloat16* orow = p.o + row * p.o_sr;
+    float* lrow = p.lse ? p.lse + row * p.l_sr : nullptr;
+    if (S2)
+        warp_merge_task_s2<D>(p.part_o, p.part_lse, p.H, s0, kvh * G, G, orow, p.o_sh, lrow, p.l_sh, lane);
+    else if (sub == 0)
+        warp_merge_group<D>(p.part_o, p.part_lse, p.H, s0, s1, kvh * G, G, orow, p.o_sh, lrow, p.l_sh, lane);
+    else
+        warp_merge_head<D>(p.part_o, p.part_lse, p.H, s0, s1, kvh * G + sub - 1, orow, p.o_sh, lrow, p.l_sh, lane);
+}
+
+int launch_merge_tasks(const spa_plan* P, void* o, int64_t o_sr, int64_t o_sh, float* lse, int64_t l_sr, int64_t l_sh,
+                       void* stream) {
+    const auto& c = P->pool->cfg;
+    const int32_t* H = P->host.data();
+    const int n_sub = H[H_N_MTASK];
+    if (n_sub == 0) return 0;
+    MergeParams mp{P->d_meta + H[H_OFF_REC_PTR], P->d_part_o, P->d_part_lse, static_cast<__nv_bfloat16*>(o), o_sr, o_sh,
+                   lse, l_sr, l_sh, H[H_N_REQ], c.num_q_heads, c.head_dim};
+    const int G = c.num_q_heads / c.num_kv_heads;
+    const dim3 grid((n_sub + 3) / 4);
+    const int32_t* m = P->d_meta;
+    if (P->merge_all_s2 && G <= 8)
+        return c.head_dim == 128
+                   ? launch_pdl(merge_tasks_kernel<128, true>, grid, dim3(128), 0, stream, m, mp, G, c.num_kv_heads)
+                   : launch_pdl(merge_tasks_kernel<64, true>, grid, dim3(128), 0, stream, m, mp, G, c.num_kv_heads);
+    return c.head_dim == 128
+               ? launch_pdl(merge_tasks_kernel<128, false>, grid, dim3(128), 0, stream, m, mp, G, c.num_kv_heads)
+               : launch_pdl(merge_tasks_kernel<64, false>, grid, dim3(128), 0, stream, m, mp, G, c.num_kv_heads);
+}
+
 int launch_merge(int32_t n_req, int32_t num_heads, int32_t head_dim, const int32_t* rec_ptr, const float* part_o,
                  const float* part_lse, void* o, int64_t o_sr, int64_t o_sh, float* lse, int64_t l_sr, int64_t l_sh,
                  int grid_hint, void* stream) {

@@ -580,10 +580,13 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
         // when there are many more head merges than warps, task * 256 + 0 (one warp merges all G heads of the task with
         // their loads in flight together: fewer, longer subtasks; needs G x S <= 32)
         const int64_t warps_total = int64_t(P->num_ctas) * P->teams * P->mt * P->kw;
-        bool whole = int64_t(tasks.size()) * G > 4 * warps_total;
+        // (the tcgen05 extend path merges with one warp per subtask in its own launch: whole tasks)
+        bool whole = P->mt == 8 || int64_t(tasks.size()) * G > 4 * warps_total;
         if (const char* e = std::getenv("SPA_MERGE_WHOLE")) whole = std::atoi(e) != 0;   // tests: force a path
+        P->merge_all_s2 = true;
         for (int32_t t : tasks) {
             const int32_t S = rec_ptr[t / Hkv + 1] - rec_ptr[t / Hkv];
+            P->merge_all_s2 = P->merge_all_s2 && whole && S == 2 && G <= 8;
             if (whole && G <= 8 && G * S <= 32 && S <= 16) {
                 mtask.push_back(t * 256);
             } else {

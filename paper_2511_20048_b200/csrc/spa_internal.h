@@ -132,6 +132,7 @@ struct spa_plan {
     spa_plan_stats stats{};
     int32_t window = 0;
     int32_t n_req = 0;
+    bool merge_all_s2 = false;  // every merge subtask is a whole (row, KV head) task of 2 records
     mutable int64_t launches = 0;  // decode launches since the last spa_decode_plan (queue slot owner ids)
     unsigned long long* trace = nullptr;   // spa_debug_set_trace: timeline buffer (device), or null
     int32_t trace_cap = 0;
@@ -186,6 +187,8 @@ struct PeerLaunch {   // F1: what the decode kernel needs to fan its outputs out
 int launch_decode(const spa_plan* plan, int32_t layer, const void* q, int64_t q_sr, int64_t q_sh, void* o,
                   int64_t o_sr, int64_t o_sh, float* lse, int64_t l_sr, int64_t l_sh, float scale, void* stream,
                   const PeerLaunch* peer = nullptr);
+int launch_merge_tasks(const spa_plan* P, void* o, int64_t o_sr, int64_t o_sh, float* lse, int64_t l_sr, int64_t l_sh,
+                       void* stream);
 int launch_merge(int32_t n_req, int32_t num_heads, int32_t head_dim, const int32_t* rec_ptr, const float* part_o,
                  const float* part_lse, void* o, int64_t o_sr, int64_t o_sh, float* lse, int64_t l_sr, int64_t l_sh,
                  int grid_hint, void* stream);

@@ -14,7 +14,7 @@ from paper_2511_20048_b200 import spa  # noqa: E402
 from spa_inputs import KIND_Q, kv_bits_torch, workloads  # noqa: E402
 
 NAMES = {10: "P issue", 11: "P rows", 12: "P K-issued", 13: "P V-free", 20: "M kfull", 21: "M S-issued", 22: "M item", 23: "M qready", 24: "M P-ready", 25: "M V-ready", 26: "M PV-issued", 30: "W sfull",
-         31: "W pfull-arr", 32: "W item", 33: "W q-written", 34: "W epi-wait", 35: "W ofull", 36: "W item-done", 37: "W S-loaded", 38: "W max-done", 39: "W exp-done", 40: "W O-rescaled", 41: "W max-only"}
+         31: "W pfull-arr", 32: "W item", 33: "W q-written", 34: "W epi-wait", 35: "W ofull", 36: "W item-done", 37: "W S-loaded", 38: "W max-done", 39: "W exp-done", 40: "W O-rescaled", 41: "W max-only", 50: "V merge-ready", 51: "W tail-merge", 52: "merge-done"}
 
 
 def main():
@@ -47,7 +47,7 @@ def main():
     spa.lib().spa_debug_set_trace(plan.h, None, 0)
     tr = buf.cpu().numpy().astype(np.uint64)
     ev = []
-    for w in range(4):
+    for w in range(5):
         for k in range(cap):
             w1 = tr[w, k, 1]
             tag = int(w1 >> np.uint64(56))
@@ -56,6 +56,14 @@ def main():
             ev.append((int(tr[w, k, 0]), w, tag, int((w1 >> np.uint64(32)) & np.uint64(0xffffff))))
     ev.sort()
     t0 = ev[0][0]
+    se = tr[7, :, :].astype(np.int64)
+    print("row 7 nonzero:", int((se != 0).sum()), se[:2].tolist())
+    se = se[(se[:, 0] > 0) & (se[:, 1] > 0)]
+    if len(se):
+        s0 = se[:, 0].min()
+        st_, en_ = (se[:, 0] - s0) / 1e3, (se[:, 1] - s0) / 1e3
+        print(f"CTAs {len(se)}: start spread {st_.max():.1f} us; end min {en_.min():.1f} median {np.median(en_):.1f} "
+              f"p90 {np.percentile(en_, 90):.1f} max {en_.max():.1f} us; busy fraction {(en_ - st_).sum() / (len(se) * en_.max()):.3f}")
     span = (ev[-1][0] - t0) / 1e3
     print(f"launch (events) {e0.elapsed_time(e1) * 1e3:.1f} us; CTA 0 trace span {span:.1f} us, {len(ev)} events")
     by = {}
@@ -114,6 +122,10 @@ def main():
     for key, v in sorted(seg.items()):
         print(f"  WG0 {NAMES.get(key[0])} -> {NAMES.get(key[1])}: n {len(v)} median {np.median(v):.0f} ns, "
               f"total {sum(v) / 1e3:.1f} us")
+    for tag, who in ((50, "V producer merges (ready tasks)"), (51, "WG0 warp tail merges")):
+        ts = [t for t, w, tg, i in ev if tg == tag]
+        if ts:
+            print(f"  {who}: {len(ts)} from {(ts[0] - t0) / 1e3:.1f} to {(ts[-1] - t0) / 1e3:.1f} us")
     print("first 60 events:")
     for t, w, tag, i in ev[:60]:
         print(f"{(t - t0):8d} ns  w{w} {NAMES.get(tag, tag):12s} {i}")
