@@ -61,7 +61,7 @@ struct DecodeParams {
 // A popped work item as the producer hands it to its team (shared memory): the item and
 // the descriptor fields the consumers need, so they do not re-read them from global memory.
 struct TeamItem {
-    int it, kv_head, n_pages, tok_start, tok_end, member_off, n_members, pad;
+    int it, kv_head, n_pages, tok_start, tok_end, member_off, n_members, n_main;   // pages >= n_main: folded tails
 };
 
 #ifndef SPA_QK_CHAINS
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8, KW_>::WARPS *
     //      lane 0 (warp-uniform).  Queue empty: publish -1, complete the barrier without data.
     int p_item = -1, p_st = 0, p_n = 0;
     bool p_done = false, p_waited = false;
-    int p_kv = 0, p_npages = 0, p_off = 0;
+    int p_kv = 0, p_npages = 0, p_off = 0, p_nmain = 0, p_kind = 0;
     int pid_base = 0, pid_cur = 0, pid_next = 0;
     auto issue_next = [&](int slot) {
         if (p_done) return;
@@ -222,13 +222,15 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8, KW_>::WARPS *
             const Item itm = items[it];
             const Desc dsc = descs[itm.desc];
             if (lane == 0) *e = TeamItem{it, itm.kv_head, dsc.n_pages, dsc.tok_start, dsc.tok_end, dsc.member_off,
-                                         dsc.n_members, 0};
+                                         dsc.n_members, dsc.n_main};
             if ((dsc.kind & 4) && !p_waited) {   // holds a newest token: wait for its producer
                 asm volatile("griddepcontrol.wait;" ::: "memory");
                 p_waited = true;
             }
             p_kv = itm.kv_head;
             p_npages = dsc.n_pages;
+            p_nmain = dsc.n_main;
+            p_kind = dsc.kind;
             p_off = dsc.page_off;
             pid_base = 0;
             pid_cur = lane < p_npages ? pages[p_off + lane] : 0;
@@ -236,6 +238,10 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8, KW_>::WARPS *
         }
         const int p0 = p_st * PPS;
         const int npg = min(PPS, p_npages - p0);
+        if ((p_kind & 8) && p0 + npg > p_nmain && !p_waited) {   // a folded tail holds a newest token
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            p_waited = true;
+        }
         int row[PPS];
 #pragma unroll
         for (int j = 0; j < PPS; ++j) {
@@ -311,6 +317,8 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8, KW_>::WARPS *
         // ---- per-row setup: member, window bound lo and causal bound hi (keys [lo, hi) are
         //      live), query fragments (padding rows: q = 0, lo = 0, hi = INT_MAX)
         int lo0 = 0, lo1 = 0, hi0 = INT_MAX, hi1 = INT_MAX;
+        // folded tails (reading #19): item pages [tk, tk + tn) are the row's own, from token tt
+        int tk0 = 0, tn0 = 0, tt0 = 0, tk1 = 0, tn1 = 0, tt1 = 0;
         uint32_t qa[KS][4];
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) qa[ks][0] = qa[ks][1] = qa[ks][2] = qa[ks][3] = 0u;
@@ -322,6 +330,9 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8, KW_>::WARPS *
                 const Member m = mems[dsc.member_off + mb];
                 lo0 = m.lo;
                 hi0 = m.hi;
+                tk0 = m.tail_k0;
+                tn0 = m.tail_n;
+                tt0 = m.tail_tok;
                 q0 = p.q + m.row * p.q_sr + (itm.kv_head * G + row0 - mb * G) * p.q_sh;
             }
             if (row1 < R) {
@@ -329,6 +340,9 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8, KW_>::WARPS *
                 const Member m = mems[dsc.member_off + mb];
                 lo1 = m.lo;
                 hi1 = m.hi;
+                tk1 = m.tail_k0;
+                tn1 = m.tail_n;
+                tt1 = m.tail_tok;
                 q1 = p.q + m.row * p.q_sr + (itm.kv_head * G + row1 - mb * G) * p.q_sh;
             }
             // fp8: the MMA's k index 2t+i (+8) reads channel 4t+i (+2) of each 16-channel block
@@ -439,8 +453,10 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8, KW_>::WARPS *
 #pragma unroll
                 for (int jj = 0; jj < JW; ++jj) {
                     const int j = wk + jj * KW;
-                    const int tokp = dsc.tok_start + (st * PPS + j) * kPageSize;
-                    const bool unmasked = (j < npg) && (tokp >= lo_warp) && (tokp + kPageSize <= hi_warp);
+                    const int kpg = st * PPS + j;   // page index within the item
+                    const bool tailp = kpg >= dsc.n_main;
+                    const int tokp = dsc.tok_start + kpg * kPageSize;
+                    const bool unmasked = !tailp && (j < npg) && (tokp >= lo_warp) && (tokp + kPageSize <= hi_warp);
                     if (unmasked) {
 #pragma unroll
                         for (int nt = 0; nt < 2; ++nt)
@@ -456,10 +472,19 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8, KW_>::WARPS *
                         for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
                             for (int e = 0; e < 4; ++e) {
-                                const int tok = tokp + nt * 8 + 2 * (lane & 3) + (e & 1);
+                                const int off = nt * 8 + 2 * (lane & 3) + (e & 1);
                                 const int lo = (e < 2) ? lo0 : lo1;
                                 const int hi = (e < 2) ? hi0 : hi1;
-                                const bool ok = (j < npg) && (tok < dsc.tok_end) && (tok >= lo) && (tok < hi);
+                                int tok;
+                                bool ok;
+                                if (!tailp) {
+                                    tok = tokp + off;
+                                    ok = (j < npg) && (tok < dsc.tok_end) && (tok >= lo) && (tok < hi);
+                                } else {   // a folded tail page: its owner's rows only
+                                    const int rel = kpg - ((e < 2) ? tk0 : tk1);
+                                    tok = ((e < 2) ? tt0 : tt1) + rel * kPageSize + off;
+                                    ok = (j < npg) && rel >= 0 && rel < ((e < 2) ? tn0 : tn1) && (tok >= lo) && (tok < hi);
+                                }
                                 const float v = ok ? s[jj][nt][e] * scale_l2 : -INFINITY;
                                 s[jj][nt][e] = v;
                                 if (e < 2) mx0 = fmaxf(mx0, v);

@@ -84,7 +84,7 @@ struct ExtParams {
 };
 
 struct ExtItem {
-    int it, kv_head, n_pages, tok_start, tok_end, member_off, n_members, kind, page_off;
+    int it, kv_head, n_pages, tok_start, tok_end, member_off, n_members, kind, page_off, n_main;
 };
 
 namespace ext {
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
             const Desc dsc = descs[itm.desc];
             if (lane == 0) {
                 *e = ExtItem{it, itm.kv_head, dsc.n_pages, dsc.tok_start, dsc.tok_end, dsc.member_off, dsc.n_members,
-                             dsc.kind, dsc.page_off};
+                             dsc.kind, dsc.page_off, dsc.n_main};
                 __threadfence_block();
                 tseq[n % QN] = n + 1;
             }
@@ -273,6 +273,10 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
                 if (st > 0) EXT_WAIT(bar(BAR_KEMPTY + ks), uint32_t(((g / NK) & 1) ^ 1), 2);
                 tr(10, st);
                 const int p0 = st * PPS, npg = min(PPS, dsc.n_pages - p0);
+                if ((dsc.kind & 8) && p0 + npg > dsc.n_main && !waited) {   // a folded tail's newest token
+                    asm volatile("griddepcontrol.wait;" ::: "memory");
+                    waited = true;
+                }
                 if (p0 >= pid_base + 32) {   // PPS divides 32: a stage never straddles a window
                     pid_base += 32;
                     pid_cur = pid_base + lane < dsc.n_pages ? pages[dsc.page_off + pid_base + lane] : 0;
@@ -334,6 +338,10 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
                 const int sl = g % nring;
                 EXT_WAIT(empty0 + sl * 8, uint32_t(((g / nring) & 1) ^ 1), 11);
                 const int p0 = st * PPS, npg = min(PPS, e.n_pages - p0);
+                if ((e.kind & 8) && p0 + npg > e.n_main && !waited) {
+                    asm volatile("griddepcontrol.wait;" ::: "memory");
+                    waited = true;
+                }
                 if (p0 >= pid_base + 32) {
                     pid_base += 32;
                     pid_cur = pid_base + lane < e.n_pages ? pages[e.page_off + pid_base + lane] : 0;
@@ -460,7 +468,7 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
         // after o_full (every S of item n has completed by then), and q_ready lets the S issuer
         // start item n + 1 while this WG's epilogue reads O; the PV issuer waits for o_free.
         struct Rows {
-            int lo, hi, mrow, rec, head;
+            int lo, hi, mrow, rec, head, tk, tn, tt;   // tk, tn, tt: folded tail (Member::tail_*)
             bool live;
         };
         auto read_entry = [&](int idx) {
@@ -473,7 +481,7 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
         auto load_rows = [&](const ExtItem& e, Rows& r, uint4* qv) {
             // padding rows attend to everything (their S is 0: Q is zero) so that their warp
             // keeps the unmasked fast path; their results are never stored
-            r = Rows{0, 0x7fffffff, 0, -1, 0, e.it >= 0 && row < e.n_members * G};
+            r = Rows{0, 0x7fffffff, 0, -1, 0, 0, 0, 0, e.it >= 0 && row < e.n_members * G};
             if (r.live) {
                 const int mb = row / G;
                 const Member m = mems[e.member_off + mb];
@@ -481,6 +489,9 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
                 r.hi = m.hi;
                 r.mrow = m.row;
                 r.rec = m.rec;
+                r.tk = m.tail_k0;
+                r.tn = m.tail_n;
+                r.tt = m.tail_tok;
                 r.head = e.kv_head * G + (row - mb * G);
                 const uint4* src = reinterpret_cast<const uint4*>(p.q + m.row * p.q_sr + r.head * p.q_sh) + wgk * 8;
 #pragma unroll
@@ -508,7 +519,7 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
         }
         while (e.it >= 0) {
             tr(32, n);
-            const int lo = rw.lo, hi = rw.hi;
+            const int lo = rw.lo, hi = rw.hi, tk = rw.tk, tn = rw.tn, tt = rw.tt;
             // a warp whose 32 rows are all padding (R <= 96 of the 128-row tile) skips its tensor-
             // memory traffic: its P / O lanes hold stale values that only feed padding rows
             const bool wdead = 32 * (warp & 3) >= e.n_members * G;
@@ -546,14 +557,29 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
                     const int tok0 = e.tok_start + st * KPS;
                     const int kmax = min(min(hi, e.tok_end), tok0 + npg * 16);   // keys [max(lo,tok0), kmax) live
                     float mx = -INFINITY;   // max of the raw logits (scale > 0 is applied in the exponent)
-                    if (tok0 >= lo && tok0 + KPS <= kmax) {
+                    if (st * PPS + npg <= e.n_main && tok0 >= lo && tok0 + KPS <= kmax) {
 #pragma unroll
                         for (int i = 0; i < KPS; ++i) mx = fmaxf(mx, s[i]);
-                    } else {
+                    } else if (st * PPS + npg <= e.n_main) {
 #pragma unroll
                         for (int i = 0; i < KPS; ++i) {
                             const int tok = tok0 + i;
                             s[i] = (tok < kmax && tok >= lo) ? s[i] : -INFINITY;
+                            mx = fmaxf(mx, s[i]);
+                        }
+                    } else {   // the stage reaches folded tail pages: their owner's rows only
+#pragma unroll
+                        for (int i = 0; i < KPS; ++i) {
+                            const int kpg = st * PPS + i / 16;
+                            bool ok;
+                            if (kpg < e.n_main) {
+                                const int tok = tok0 + i;
+                                ok = tok < kmax && tok >= lo;
+                            } else {
+                                const int rel = kpg - tk, tok = tt + rel * 16 + (i & 15);
+                                ok = i < npg * 16 && rel >= 0 && rel < tn && tok >= lo && tok < hi;
+                            }
+                            s[i] = ok ? s[i] : -INFINITY;
                             mx = fmaxf(mx, s[i]);
                         }
                     }

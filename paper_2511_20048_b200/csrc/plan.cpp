@@ -31,12 +31,19 @@ void plan_release(spa_plan* P);               // kernels.cu
 
 namespace {
 
+struct Fold {                  // a member tail read by its host range's last descriptor
+    std::vector<int> rows;
+    int32_t a, b;
+    const std::vector<int32_t>* table;
+};
+
 struct Range {
     int kind;                 // bit 0: a row of the range also reads another range (partial records)
     int group;
     std::vector<int> members; // batch rows
     int32_t a, b;             // tokens [a, b)
     const std::vector<int32_t>* table;
+    std::vector<Fold> folds;  // member tails appended to the range's last descriptor
 };
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -367,7 +374,7 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
                 for (int x = ufirst[u]; x < urow_end[u]; ++x)
                     if (lo[x] < b && V[x].hi > a) rows.push_back(x);
             std::sort(rows.begin(), rows.end());
-            classes.push_back(Range{r.reqs.size() > 1 ? 0 : 1, gid, std::move(rows), a, b, &table(r.reqs[0])});
+            classes.push_back(Range{r.reqs.size() > 1 ? 0 : 1, gid, std::move(rows), a, b, &table(r.reqs[0]), {}});
         }
     }
 
@@ -391,7 +398,7 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
             std::vector<int> chunk(c.members.begin() + c0,
                                    c.members.begin() + std::min(c.members.size(), c0 + max_members));
             // chunk rows may span requests: the page list is the same for all of them
-            ranges.push_back(Range{c.kind, c.group, std::move(chunk), c.a, c.b, c.table});
+            ranges.push_back(Range{c.kind, c.group, std::move(chunk), c.a, c.b, c.table, {}});
         }
     }
 
@@ -409,16 +416,25 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
 
     // every page a range reads must be resident (spa_kv_release_window leaves -1 entries; a
     // plan whose window reaches back into them is the caller's error)
-    for (const auto& r : ranges)
+    for (const auto& r : ranges) {
         for (int32_t p = r.a / ps; p < int32_t(cdiv(r.b, ps)); ++p)
             if ((*r.table)[p] < 0)
                 return fail(SPA_ERR_INVALID_ARG, "plan: a request's window needs a page released by spa_kv_release_window");
+        for (const auto& f : r.folds)
+            for (int32_t p = f.a / ps; p < int32_t(cdiv(f.b, ps)); ++p)
+                if ((*f.table)[p] < 0)
+                    return fail(SPA_ERR_INVALID_ARG, "plan: a request's window needs a page released by spa_kv_release_window");
+    }
 
     // ---- 3. split size
     int64_t total_pages = 0;
     for (const auto& r : ranges) {
         unique_tokens += r.b - r.a;
         total_pages += cdiv(r.b, ps) - r.a / ps;
+        for (const auto& f : r.folds) {
+            unique_tokens += f.b - f.a;
+            total_pages += cdiv(f.b, ps) - f.a / ps;
+        }
     }
     static const int max_splits =
         std::getenv("SPA_MAX_SPLITS") ? std::max(1, std::atoi(std::getenv("SPA_MAX_SPLITS"))) : kMaxSplits;
@@ -448,8 +464,10 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
                     const int32_t Cr = std::max<int32_t>(Cf, int32_t(cdiv(pb - pa, max_splits)));
                     const int32_t n = int32_t(cdiv(pb - pa, Cr));
                     const double rows = double(r.members.size() * G);
+                    int32_t fold_pages = 0;
+                    for (const auto& f : r.folds) fold_pages += int32_t(cdiv(f.b, ps) - f.a / ps);
                     for (int32_t s = 0; s < n; ++s) {
-                        const int32_t np = std::min(Cr, pb - pa - s * Cr);
+                        const int32_t np = std::min(Cr, pb - pa - s * Cr) + (s == n - 1 ? fold_pages : 0);
                         const double c = np + 1 + (n > 1 || r.kind ? rows / 16.0 : 0.0);
                         for (int h = 0; h < Hkv; ++h) costs.push_back(c);
                     }
@@ -477,6 +495,66 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
         C = std::max(4, std::min(C, 1 << 20));
     }
 
+    // cut points of a range: pieces of Cr pages, at most kMaxSplits splits per range (a
+    // request then has <= 2 kMaxSplits partial records, shared + tail, which the merge reads in
+    // chunks of 16 per L2 round trip), except that (automatic splits) the last tail_frac of a
+    // long range is cut into pieces of Cr / tail_div pages.  The largest-first queue hands
+    // those out last, so teams that finish early fill the end of the launch instead of idling
+    // while slower teams finish their big pieces.
+    auto cuts_of = [&](const Range& r) {
+        const int32_t pa = r.a / ps, pb = int32_t(cdiv(r.b, ps));
+        const int32_t Cr = P->cfg.split_pages > 0 ? C : std::max<int32_t>(C, int32_t(cdiv(pb - pa, max_splits)));
+        std::vector<int32_t> cuts{pa};
+        int32_t main_end = pb;
+        const int32_t small = std::max<int32_t>(4, int32_t(cdiv(Cr, tail_div)));
+        if (P->cfg.split_pages <= 0 && tail_frac > 0 && pb - pa >= 2 * small) {
+            const int32_t tail = std::max<int32_t>(small, int32_t(std::lround((pb - pa) * tail_frac)));
+            main_end = pb - std::min(tail, pb - pa - small);
+        }
+        for (int32_t s = pa + Cr; s < main_end; s += Cr) cuts.push_back(s);
+        if (main_end > cuts.back()) cuts.push_back(main_end);
+        for (int32_t s = main_end + small; s < pb; s += small) cuts.push_back(s);
+        if (cuts.back() != pb) cuts.push_back(pb);
+        return cuts;
+    };
+
+    // ---- 3b. fold member tails (reading #19): a range read by the rows of ONE request (its
+    //      private tail: a speculative prompt, a parent's newest tokens) whose first page
+    //      directly follows an UNSPLIT shared range holding all of those rows is appended to
+    //      that range's descriptor instead of being a work item of its own: its pages are read
+    //      once as before, but by the item that already holds the rows' softmax state, so the
+    //      rows need no partial record and no split merge, and no tiny tail item costs a
+    //      pipeline refill and an epilogue.  (A split host would keep its rows' records anyway;
+    //      folding there only lengthens its last piece -- measured slower.)  The kernels mask
+    //      a folded page for every row but its owner's.
+    static const bool fold_tails = !std::getenv("SPA_FOLD") || std::atoi(std::getenv("SPA_FOLD")) != 0;
+    if (fold_tails && P->cfg.sharing) {
+        std::vector<char> dead(ranges.size(), 0);
+        for (size_t t = 0; t < ranges.size(); ++t) {
+            const Range& T = ranges[t];
+            const Request* owner = V[T.members[0]].req;
+            bool one = true;
+            for (int m : T.members) one = one && V[m].req == owner;
+            if (!one || !T.folds.empty()) continue;
+            for (size_t h = 0; h < ranges.size(); ++h) {
+                Range& Hr = ranges[h];
+                if (h == t || dead[h] || Hr.group != T.group || int32_t(cdiv(Hr.b, ps)) != T.a / ps) continue;
+                if (cuts_of(Hr).size() != 2) continue;   // split host: keep the tail an item
+                bool multi = false, holds = true;
+                for (int m : Hr.members) multi = multi || V[m].req != owner;
+                for (int m : T.members) holds = holds && std::find(Hr.members.begin(), Hr.members.end(), m) != Hr.members.end();
+                if (!multi || !holds) continue;
+                Hr.folds.push_back(Fold{T.members, T.a, T.b, T.table});
+                dead[t] = 1;
+                break;
+            }
+        }
+        std::vector<Range> kept;
+        for (size_t t = 0; t < ranges.size(); ++t)
+            if (!dead[t]) kept.push_back(std::move(ranges[t]));
+        ranges.swap(kept);
+    }
+
     // ---- 4. descriptors, members, pages
     std::vector<Desc> descs;
     std::vector<Member> members;
@@ -484,27 +562,8 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
     std::vector<int32_t> occ(n_req, 0);
     int64_t pages_read = 0;
     for (const auto& r : ranges) {
-        const int32_t pa = r.a / ps, pb = int32_t(cdiv(r.b, ps));
-        // at most kMaxSplits splits per range: a request then has <= 2 kMaxSplits partial
-        // records (shared + tail), which the merge reads in chunks of 16 per L2 round trip
-        const int32_t Cr = P->cfg.split_pages > 0 ? C : std::max<int32_t>(C, int32_t(cdiv(pb - pa, max_splits)));
-        // cut points: pieces of Cr pages, except that (automatic splits) the last tail_frac of
-        // a long range is cut into pieces of Cr / tail_div pages.  The largest-first queue
-        // hands those out last, so teams that finish early fill the end of the launch
-        // instead of idling while slower teams finish their big pieces.
-        std::vector<int32_t> cuts{pa};
-        {
-            int32_t main_end = pb;
-            const int32_t small = std::max<int32_t>(4, int32_t(cdiv(Cr, tail_div)));
-            if (P->cfg.split_pages <= 0 && tail_frac > 0 && pb - pa >= 2 * small) {
-                const int32_t tail = std::max<int32_t>(small, int32_t(std::lround((pb - pa) * tail_frac)));
-                main_end = pb - std::min(tail, pb - pa - small);
-            }
-            for (int32_t s = pa + Cr; s < main_end; s += Cr) cuts.push_back(s);
-            if (main_end > cuts.back()) cuts.push_back(main_end);
-            for (int32_t s = main_end + small; s < pb; s += small) cuts.push_back(s);
-            if (cuts.back() != pb) cuts.push_back(pb);
-        }
+        const int32_t pa = r.a / ps;
+        const std::vector<int32_t> cuts = cuts_of(r);
         for (size_t ci = 0; ci + 1 < cuts.size(); ++ci) {
             const int32_t s = cuts[ci], e = cuts[ci + 1];
             Desc d{};
@@ -521,10 +580,27 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
             for (int m : r.members)
                 if (d.tok_end > V[m].first_new) d.kind |= 4;
             d.group = r.group;
+            d.n_main = d.n_pages;
             for (int32_t p = s; p < e; ++p) pages.push_back((*r.table)[p]);
             for (int m : r.members) {
-                members.push_back(Member{m, lo[m], 0, V[m].hi});
+                members.push_back(Member{m, lo[m], 0, V[m].hi, 0, 0, 0, 0});
                 occ[m] += 1;
+            }
+            if (ci + 2 == cuts.size()) {   // the range's last descriptor takes its folded tails
+                for (const auto& f : r.folds) {
+                    const int32_t fa = f.a / ps, fb = int32_t(cdiv(f.b, ps));
+                    for (int m : f.rows) {
+                        for (int32_t mi = d.member_off; mi < d.member_off + d.n_members; ++mi)
+                            if (members[mi].row == m) {
+                                members[mi].tail_k0 = d.n_pages;
+                                members[mi].tail_n = fb - fa;
+                                members[mi].tail_tok = fa * ps;
+                            }
+                        if (f.b > V[m].first_new) d.kind |= 8;
+                    }
+                    for (int32_t p = fa; p < fb; ++p) pages.push_back((*f.table)[p]);
+                    d.n_pages += fb - fa;
+                }
             }
             descs.push_back(d);
             pages_read += d.n_pages;
@@ -604,8 +680,8 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
         H.insert(H.end(), w, w + words);
         while (H.size() % 4) H.push_back(0);   // 16-B alignment of every array
     };
-    put(H_OFF_DESC, descs.data(), descs.size() * 8);
-    put(H_OFF_MEMBER, members.data(), members.size() * 4);
+    put(H_OFF_DESC, descs.data(), descs.size() * (sizeof(Desc) / 4));
+    put(H_OFF_MEMBER, members.data(), members.size() * (sizeof(Member) / 4));
     put(H_OFF_ITEM, items.data(), items.size() * 2);
     while (H.size() % 32) H.push_back(0);   // 128-B lines: the queue heads are hot atomics
     put(H_OFF_SCHED, sched.data(), sched.size());
@@ -696,8 +772,8 @@ spa_status spa_plan_debug_array(const spa_plan* plan, int32_t which, const int32
     int slot = 0, width = 1;
     int64_t n = 0;
     switch (which) {
-        case SPA_DBG_DESC: slot = H_OFF_DESC; width = 8; n = H[H_N_DESC]; break;
-        case SPA_DBG_MEMBER: slot = H_OFF_MEMBER; width = 4; n = H[H_N_MEMBERS]; break;
+        case SPA_DBG_DESC: slot = H_OFF_DESC; width = int(sizeof(Desc) / 4); n = H[H_N_DESC]; break;
+        case SPA_DBG_MEMBER: slot = H_OFF_MEMBER; width = int(sizeof(Member) / 4); n = H[H_N_MEMBERS]; break;
         case SPA_DBG_ITEM: slot = H_OFF_ITEM; width = 2; n = H[H_N_ITEMS]; break;
         case SPA_DBG_QUEUE: slot = H_OFF_QUEUE; n = H[H_N_ITEMS]; break;
         case SPA_DBG_PAGES: slot = H_OFF_PAGES; n = H[H_N_PAGES]; break;

@@ -43,12 +43,17 @@ enum MetaHeader : int {
     H_WORDS = 20
 };
 
-// Work descriptor: keys [tok_start, tok_end) of one group-split or member-tail-split,
-// read through pages[page_off .. page_off + n_pages) (tok_start = first page * ps).
+// Work descriptor: keys [tok_start, tok_end) of one group-split or member-tail-split, read
+// through pages[page_off .. page_off + n_main) (tok_start = first page * ps), then (folded
+// member tails) pages [n_main, n_pages) of the same list: each member's own tail, read only
+// by that member's rows (Member::tail_*).  kind: bit 0 some row also reads another
+// descriptor; bit 2 the shared pages hold a member's newest token; bit 3 a folded tail does
+// (the kernels do not prefetch such pages before their programmatic-dependency wait).
 struct Desc {
     int32_t page_off, n_pages, tok_start, tok_end, member_off, n_members, kind, group;
+    int32_t n_main, reserved0, reserved1, reserved2;
 };
-static_assert(sizeof(Desc) == 32, "Desc is 8 int32");
+static_assert(sizeof(Desc) == 48, "Desc is 12 int32");
 
 // One request (batch row) taking part in a descriptor.
 struct Member {
@@ -56,6 +61,9 @@ struct Member {
     int32_t lo;    // window lower bound: keys j < lo are masked for this member
     int32_t rec;   // partial record index, or -1: write final O / LSE directly
     int32_t hi;    // causal bound: keys j >= hi are masked for this row (decode: the length)
+    // folded tail: descriptor pages [tail_k0, tail_k0 + tail_n) are this row's own, page
+    // tail_k0 holding its tokens [tail_tok, tail_tok + ps); tail_n = 0: none
+    int32_t tail_k0, tail_n, tail_tok, reserved;
 };
 
 struct Item {

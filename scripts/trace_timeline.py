@@ -1,6 +1,6 @@
 """Timeline of one decode launch (spa_debug_set_trace): where a launch's time goes.
 
-    python scripts/trace_timeline.py [qwen | sweep:B:f | long] [--teams N] [--split P] [--out file.json]
+    python scripts/trace_timeline.py [qwen | sweep:B:f | long | gemma] [--window W] [--teams N] [--split P] [--out file.json]
 
 Runs the workload PDL-chained over 8 resident layers (as the bench chains layer calls),
 traces the last launch and prints: entry spread, ramp (first item start per team), busy
@@ -135,7 +135,8 @@ def main():
     ap.add_argument("--merge", type=int, default=0)
     ap.add_argument("--out", default=None)
     ap.add_argument("--kv", default="bf16", choices=["bf16", "fp8"])
-    ap.add_argument("--rows", type=int, default=16, help="plan max_rows (16, 32, 64)")
+    ap.add_argument("--rows", type=int, default=16, help="plan max_rows (0 auto, 16, 32, 64)")
+    ap.add_argument("--window", type=int, default=0, help="sliding window (gemma local layers: 1024)")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     stream = torch.cuda.Stream()
@@ -144,6 +145,8 @@ def main():
         rec = workloads.qwen()
     elif a.workload == "long":
         rec = workloads.long32k()
+    elif a.workload == "gemma":
+        rec = workloads.gemma()
     else:
         _, b, f = a.workload.split(":")
         rec = workloads.sweep(int(b), float(f))
@@ -158,7 +161,7 @@ def main():
     o = torch.empty((Lr, N, m.num_q_heads, m.head_dim), dtype=torch.bfloat16, device=dev)
     lse = torch.empty((Lr, N, m.num_q_heads), dtype=torch.float32, device=dev)
     plan = spa.Plan(pool, split_pages=a.split, merge_mode=a.merge, teams_per_cta=a.teams, max_rows=a.rows)
-    plan.plan(reqs, 0, stream=stream)
+    plan.plan(reqs, a.window, stream=stream)
     st = plan.stats()
 
     def run(n):
@@ -180,12 +183,12 @@ def main():
     host_us = (h1 - h0) / calls * 1e6
     # CUDA graph of `calls` chained launches (the plan's launch counter advances in capture)
     g = torch.cuda.CUDAGraph()
-    plan.plan(reqs, 0, stream=stream)
+    plan.plan(reqs, a.window, stream=stream)
     with torch.cuda.graph(g, stream=stream):
         run(calls)
     graph_us = []
     for _ in range(5):
-        plan.plan(reqs, 0, stream=stream)   # resets the launch ids the graph was captured with
+        plan.plan(reqs, a.window, stream=stream)   # resets the launch ids the graph was captured with
         torch.cuda.synchronize()
         e0.record(stream)
         g.replay()
@@ -193,7 +196,7 @@ def main():
         torch.cuda.synchronize()
         graph_us.append(e0.elapsed_time(e1) / calls * 1e3)
     # trace the last of 8 chained launches
-    plan.plan(reqs, 0, stream=stream)
+    plan.plan(reqs, a.window, stream=stream)
     run(7)
     buf = plan.set_trace(256)   # zeroed on the stream; the traced launch follows 7 chained ones
     plan.decode(7 % Lr, q[7 % Lr], o[7 % Lr], lse[7 % Lr], scale=m.softmax_scale, stream=stream)

@@ -56,11 +56,13 @@ def check_plan(pool, plan, reqs, window, n_query=None):
     cover = [dict() for _ in range(N)]   # token -> count
     occ = [0] * N
     recs = [[] for _ in range(N)]
-    for d in descs:
-        page_off, n_pages, t0, t1, moff, nmem, kind, group = d
-        assert t0 % 16 == 0 and t1 <= t0 + 16 * n_pages and t1 > t0 + 16 * (n_pages - 1)
+    tail_owner = {}   # (descriptor, folded page index) -> owning row (one request's rows only)
+    for di, d in enumerate(descs):
+        page_off, n_pages, t0, t1, moff, nmem, kind, group, n_main = d[:9]
+        # shared pages [0, n_main) hold keys [t0, t1); folded member tails follow (reading #19)
+        assert t0 % 16 == 0 and t1 <= t0 + 16 * n_main and t1 > t0 + 16 * (n_main - 1)
         for mi in range(moff, moff + nmem):
-            row, lo, rec, hi = mems[mi]
+            row, lo, rec, hi, tk0, tn, ttok, _ = mems[mi]
             occ[row] += 1
             recs[row].append(rec)
             tab = row_tab[row]
@@ -68,6 +70,15 @@ def check_plan(pool, plan, reqs, window, n_query=None):
             for t in range(max(t0, lo), min(t1, hi)):
                 assert pages[page_off + (t - t0) // 16] == tab[t // 16], "wrong physical page"
                 cover[row][t] = cover[row][t] + 1 if t in cover[row] else 1
+            if tn:
+                assert n_main <= tk0 and tk0 + tn <= n_pages and ttok % 16 == 0 and ttok >= t1
+                for k in range(tk0, tk0 + tn):   # a folded page belongs to one request
+                    prev = tail_owner.setdefault((di, k), row)
+                    assert prev == row or row_tab[prev] is tab
+                for t in range(max(ttok, lo), min(ttok + 16 * tn, hi)):
+                    assert pages[page_off + tk0 + (t - ttok) // 16] == tab[t // 16], "wrong folded page"
+                    cover[row][t] = cover[row][t] + 1 if t in cover[row] else 1
+        assert all((di, k) in tail_owner for k in range(n_main, n_pages)), "a folded page nobody owns"
     for r in range(N):
         assert sorted(cover[r]) == list(range(row_lo[r], row_hi[r])), r
         assert all(c == 1 for c in cover[r].values())
