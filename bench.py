@@ -93,12 +93,15 @@ def peaks():
 
 
 def layer_schedule(recipe, resident):
-    """[(resident layer, window)] of the attention calls of one model step."""
+    """[(resident layer, window)] of the attention calls of one model step: one call per model
+    layer (S8(d): a step is the whole model's attention), cycling through the resident layers
+    when the pool holds fewer (Gemma-3: 62 calls over 6; long-32k: 64 calls over 4 -- each
+    call reads more than the L2 holds, so a re-used resident layer is not served from cache)."""
     m = recipe.model
     if recipe.local_layers:
         local = set(recipe.local_layers)
         return [(i % resident, recipe.window if i in local else 0) for i in range(m.num_layers)]
-    return [(i, 0) for i in range(resident)]
+    return [(i % resident, 0) for i in range(m.num_layers)]
 
 
 # ----------------------------------------------------------------------------- oracle (cpu)

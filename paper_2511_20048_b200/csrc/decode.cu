@@ -172,10 +172,9 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8, KW_>::WARPS *
     tr(1, 0);
 
     const int32_t* meta = p.meta;
-    const Desc* descs = reinterpret_cast<const Desc*>(meta + meta[H_OFF_DESC]);
+    const QItem* qitems = reinterpret_cast<const QItem*>(meta + meta[H_OFF_QITEM]);
     const Member* mems = reinterpret_cast<const Member*>(meta + meta[H_OFF_MEMBER]);
-    const Item* items = reinterpret_cast<const Item*>(meta + meta[H_OFF_ITEM]);
-    const int32_t* queue = meta + meta[H_OFF_QUEUE];
+
     const int32_t* pages = meta + meta[H_OFF_PAGES];
     const int32_t* rec_ptr = meta + meta[H_OFF_REC_PTR];
     int32_t* counters = const_cast<int32_t*>(meta) + meta[H_OFF_COUNTERS];
@@ -206,7 +205,9 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8, KW_>::WARPS *
                 qi = atomicAdd(sched, 1);
             }
             qi = __shfl_sync(0xffffffffu, qi, 0);
-            const int it = qi < n_items ? queue[qi] : -1;
+            const bool live_q = qi < n_items;
+            const QItem qe = live_q ? qitems[qi] : QItem{};
+            const int it = live_q ? qe.it : -1;
             TeamItem* e = &tq[p_n % C::QN];
             ++p_n;
             if (it < 0) {
@@ -219,15 +220,15 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8, KW_>::WARPS *
             }
             p_item = it;
             p_st = 0;
-            const Item itm = items[it];
-            const Desc dsc = descs[itm.desc];
-            if (lane == 0) *e = TeamItem{it, itm.kv_head, dsc.n_pages, dsc.tok_start, dsc.tok_end, dsc.member_off,
+            const Desc& dsc = qe.d;
+            const int kvh = qe.kv_head;
+            if (lane == 0) *e = TeamItem{it, kvh, dsc.n_pages, dsc.tok_start, dsc.tok_end, dsc.member_off,
                                          dsc.n_members, dsc.n_main};
             if ((dsc.kind & 4) && !p_waited) {   // holds a newest token: wait for its producer
                 asm volatile("griddepcontrol.wait;" ::: "memory");
                 p_waited = true;
             }
-            p_kv = itm.kv_head;
+            p_kv = kvh;
             p_npages = dsc.n_pages;
             p_nmain = dsc.n_main;
             p_kind = dsc.kind;
@@ -363,6 +364,12 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8, KW_>::WARPS *
 #pragma unroll
                     for (int e = 0; e < 4; ++e) qa[ks][e] = bf16x2_to_f16x2(qa[ks][e]);
             }
+        }
+        if (trace) {   // timeline: the row setup's loads have landed
+            uint32_t d0 = qa[0][0] | qa[KS - 1][3] | uint32_t(lo0) | uint32_t(tk1);
+            asm volatile("mov.b32 %0, %0;" : "+r"(d0));
+            if (d0 == 0x9e3779b9u) tr(12, 0);
+            tr(9, it);
         }
         // keys in [lo_warp, hi_warp) are live for every row of the warp: such pages need no mask
         int lo_warp = max(lo0, lo1), hi_warp = min(hi0, hi1);
@@ -580,6 +587,7 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8, KW_>::WARPS *
             if (producer) {
                 mbar_wait(empty_bar(slot), phase);   // acquire: both warps are past the stage
                 if (pend_nm) {
+                    tr(11, 0);
                     count_records();
                     tr(8, 0);
                 }
@@ -591,6 +599,7 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8, KW_>::WARPS *
             }
         }
 
+        tr(10, it);
         // ---- epilogue (KW = 1): the warp holds its row tile's whole state; normalise and
         //      write every column
         if constexpr (KW == 1) {
@@ -655,7 +664,9 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8, KW_>::WARPS *
             };
             if (wk == 0) publish(comb + 16 * (D / 2), acc + NTH);
             else publish(comb, acc);
+            tr(13, 0);
             pair_sync();
+            tr(14, 0);
             const int ow = 1 - wk;
             const float om0 = ml[(ow * 16 + r0) * 2 + 0], ol0 = ml[(ow * 16 + r0) * 2 + 1];
             const float om1 = ml[(ow * 16 + r0 + 8) * 2 + 0], ol1 = ml[(ow * 16 + r0 + 8) * 2 + 1];
@@ -681,6 +692,7 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8, KW_>::WARPS *
             if (wk == 0) gather(comb, acc);
             else gather(comb + 16 * (D / 2), acc + NTH);
             pair_sync();   // the exchange buffers may be rewritten by the next item
+            tr(15, 0);
 #pragma unroll
             for (int rr = 0; rr < 2; ++rr) {
                 const int row = rr ? row1 : row0;

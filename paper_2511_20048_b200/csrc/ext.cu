@@ -208,10 +208,9 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
     };
 
     const int32_t* meta = p.meta;
-    const Desc* descs = reinterpret_cast<const Desc*>(meta + meta[H_OFF_DESC]);
+    const QItem* qitems = reinterpret_cast<const QItem*>(meta + meta[H_OFF_QITEM]);
     const Member* mems = reinterpret_cast<const Member*>(meta + meta[H_OFF_MEMBER]);
-    const Item* items = reinterpret_cast<const Item*>(meta + meta[H_OFF_ITEM]);
-    const int32_t* queue = meta + meta[H_OFF_QUEUE];
+
     const int32_t* pages = meta + meta[H_OFF_PAGES];
     int32_t* sched = const_cast<int32_t*>(meta) + meta[H_OFF_SCHED] + kSchedStride * (p.launch % kSchedSlots);
     const int n_items = meta[H_N_ITEMS];
@@ -238,7 +237,8 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
                 qi = atomicAdd(sched, 1);
             }
             qi = __shfl_sync(0xffffffffu, qi, 0);
-            const int it = qi < n_items ? queue[qi] : -1;
+            const QItem qe = qi < n_items ? qitems[qi] : QItem{};
+            const int it = qi < n_items ? qe.it : -1;
             ExtItem* e = &tq[n % QN];
             // the K slot of this item's first stage (or the end marker): its fill publishes the
             // entry to the MMA warp and the softmax WGs; tseq publishes it to the followers
@@ -252,8 +252,8 @@ __global__ void __launch_bounds__(ext::THREADS, 1)
                 }
                 break;
             }
-            const Item itm = items[it];
-            const Desc dsc = descs[itm.desc];
+            const Desc& dsc = qe.d;
+            const Item itm{qe.desc, qe.kv_head};
             if (lane == 0) {
                 *e = ExtItem{it, itm.kv_head, dsc.n_pages, dsc.tok_start, dsc.tok_end, dsc.member_off, dsc.n_members,
                              dsc.kind, dsc.page_off, dsc.n_main};

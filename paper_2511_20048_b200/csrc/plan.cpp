@@ -686,6 +686,15 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
     while (H.size() % 32) H.push_back(0);   // 128-B lines: the queue heads are hot atomics
     put(H_OFF_SCHED, sched.data(), sched.size());
     put(H_OFF_QUEUE, order.data(), order.size());
+    {
+        std::vector<QItem> qitems(order.size());
+        for (size_t qi = 0; qi < order.size(); ++qi) {
+            const Item& itm = items[order[qi]];
+            qitems[qi] = QItem{descs[itm.desc], order[qi], itm.kv_head, itm.desc, 0};
+        }
+        while (H.size() % 16) H.push_back(0);   // 64-B aligned entries
+        put(H_OFF_QITEM, qitems.data(), qitems.size() * (sizeof(QItem) / 4));
+    }
     put(H_OFF_PAGES, pages.data(), pages.size());
     put(H_OFF_REC_PTR, rec_ptr.data(), rec_ptr.size());
     {

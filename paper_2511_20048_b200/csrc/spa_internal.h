@@ -40,6 +40,7 @@ enum MetaHeader : int {
     H_OFF_MTASK = 16,      // int32 [n_mtask]: tail-merge subtasks (row * Hkv + kv_head) * 256 + (0: all G
                            // heads | 1 + head), earliest-ready first
     H_N_MTASK = 17,
+    H_OFF_QITEM = 18,      // QItem[n_items]: the queue's items with their descriptors, in pop order
     H_WORDS = 20
 };
 
@@ -69,6 +70,15 @@ struct Member {
 struct Item {
     int32_t desc, kv_head;
 };
+
+// A queue entry as the kernels pop it: the item's descriptor copied next to its KV head, so
+// a pop is one atomic and one 64-B load instead of four dependent loads (queue -> item ->
+// descriptor)
+struct QItem {
+    Desc d;
+    int32_t it, kv_head, desc, reserved;
+};
+static_assert(sizeof(QItem) == 64, "QItem is 16 int32");
 
 constexpr int kPageSize = 16;          // tokens per page the kernels implement
 constexpr int kPagesPerStage = 2;      // pages of one (KV head) streamed per pipeline stage

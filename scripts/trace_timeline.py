@@ -124,6 +124,35 @@ def analyse(tr, n_items_cost=None):
     out["tail_entry_even_odd_us"] = [float(np.nanmedian(tin[0::2])), float(np.nanmedian(tin[1::2]))]
     out["items_per_team"] = [int(x) for x in np.percentile([(tag[t] == 2).sum() for t in range(tr.shape[0])],
                                                             [0, 50, 100])]
+    # per-item phases of every traced warp: start (2) -> row setup landed (9) -> pages done (10)
+    # -> epilogue done (3); record-count fence (11 -> 8)
+    ph = {"setup": [], "pages": [], "epilogue": [], "count_fence": []}
+    for t in range(tr.shape[0]):
+        tg, tt = tag[t], rel[t]
+        for k in range(len(tg)):
+            if tg[k] == 2 and k + 3 < len(tg):
+                seq = {}
+                for j in range(k + 1, min(len(tg), k + 8)):
+                    if tg[j] in (9, 10, 3) and tg[j] not in seq:
+                        seq[tg[j]] = tt[j]
+                    if tg[j] == 3:
+                        break
+                if 9 in seq and 10 in seq and 3 in seq:
+                    ph["setup"].append(seq[9] - tt[k])
+                    ph["pages"].append(seq[10] - seq[9])
+                    ph["epilogue"].append(seq[3] - seq[10])
+            if tg[k] == 11 and k + 1 < len(tg) and tg[k + 1] == 8:
+                ph["count_fence"].append(tt[k + 1] - tt[k])
+            if tg[k] == 10 and k + 1 < len(tg) and tg[k + 1] == 13:
+                ph["epi_publish"] = ph.get("epi_publish", []) + [tt[k + 1] - tt[k]]
+            if tg[k] == 13 and k + 1 < len(tg) and tg[k + 1] == 14:
+                ph["epi_pair_wait"] = ph.get("epi_pair_wait", []) + [tt[k + 1] - tt[k]]
+            if tg[k] == 14 and k + 1 < len(tg) and tg[k + 1] == 15:
+                ph["epi_gather"] = ph.get("epi_gather", []) + [tt[k + 1] - tt[k]]
+            if tg[k] == 15 and k + 1 < len(tg) and tg[k + 1] == 3:
+                ph["epi_store"] = ph.get("epi_store", []) + [tt[k + 1] - tt[k]]
+    out["item_phases_us"] = {k: ([float(np.percentile(v, q)) for q in (10, 50, 90)] + [float(np.sum(v) / tr.shape[0])])
+                             for k, v in ph.items() if v}   # p10, p50, p90, total per warp
     return out
 
 
