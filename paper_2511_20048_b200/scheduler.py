@@ -204,8 +204,12 @@ def _lstsq(rows, y):
     return x
 
 
-def calibrate(table, max_rel_err: float = 0.10):
+def calibrate(table, max_rel_err: float = 0.10, relative: bool = False):
     """Least-squares fit of the T_h parameters on a profile table.
+    relative=True minimises relative instead of absolute residuals (each row weighted by
+    1 / seconds; reading F3-b): a measured table spanning 1 to 256 decode requests
+    covers two orders of magnitude of step time, where absolute least squares leaves the
+    small batches with large relative errors.
 
     table: rows (prefill_len, prefill_count, decode_count, seconds[, fork_count]).  The
     knee N0 is chosen among the table's decode counts (and "no knee") by residual; for each
@@ -233,8 +237,9 @@ def calibrate(table, max_rel_err: float = 0.10):
             feats = [1.0, min(nd, n0) + ex_m, ex_m, pc, pc * pl]
             if with_forks:
                 feats += [nf, ex_f]
-            X.append(feats)
-            y.append(sec)
+            wgt = 1.0 / sec if relative else 1.0
+            X.append([f * wgt for f in feats])
+            y.append(sec * wgt)
         try:
             x = _lstsq(X, y)
         except CalibrationError:
@@ -252,8 +257,8 @@ def calibrate(table, max_rel_err: float = 0.10):
             continue
         errs = [abs(hybrid_batch_time([(pl, pc)] if pc else (), nd, params, fork_count=nf) - sec) / sec
                 for (pl, pc, nd, sec, nf) in rows]
-        sse = sum((hybrid_batch_time([(pl, pc)] if pc else (), nd, params, fork_count=nf) - sec) ** 2
-                  for (pl, pc, nd, sec, nf) in rows)
+        sse = sum(((hybrid_batch_time([(pl, pc)] if pc else (), nd, params, fork_count=nf) - sec) /
+                   (sec if relative else 1.0)) ** 2 for (pl, pc, nd, sec, nf) in rows)
         if best is None or sse < best[0]:
             best = (sse, params, errs)
     if best is None:
