@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8, KW_>::WARPS *
         // ---- per-row setup: member, window bound lo and causal bound hi (keys [lo, hi) are
         //      live), query fragments (padding rows: q = 0, lo = 0, hi = INT_MAX)
         int lo0 = 0, lo1 = 0, hi0 = INT_MAX, hi1 = INT_MAX;
-        // folded tails (reading #19): item pages [tk, tk + tn) are the row's own, from token tt
+        // folded tails (reading #21): item pages [tk, tk + tn) are the row's own, from token tt
         int tk0 = 0, tn0 = 0, tt0 = 0, tk1 = 0, tn1 = 0, tt1 = 0;
         uint32_t qa[KS][4];
 #pragma unroll

@@ -518,7 +518,7 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
         return cuts;
     };
 
-    // ---- 3b. fold member tails (reading #19): a range read by the rows of ONE request (its
+    // ---- 3b. fold member tails (reading #21): a range read by the rows of ONE request (its
     //      private tail: a speculative prompt, a parent's newest tokens) whose first page
     //      directly follows an UNSPLIT shared range holding all of those rows is appended to
     //      that range's descriptor instead of being a work item of its own: its pages are read

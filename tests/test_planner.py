@@ -59,7 +59,7 @@ def check_plan(pool, plan, reqs, window, n_query=None):
     tail_owner = {}   # (descriptor, folded page index) -> owning row (one request's rows only)
     for di, d in enumerate(descs):
         page_off, n_pages, t0, t1, moff, nmem, kind, group, n_main = d[:9]
-        # shared pages [0, n_main) hold keys [t0, t1); folded member tails follow (reading #19)
+        # shared pages [0, n_main) hold keys [t0, t1); folded member tails follow (reading #21)
         assert t0 % 16 == 0 and t1 <= t0 + 16 * n_main and t1 > t0 + 16 * (n_main - 1)
         for mi in range(moff, moff + nmem):
             row, lo, rec, hi, tk0, tn, ttok, _ = mems[mi]
