@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8, KW_>::WARPS *
     bool p_done = false, p_waited = false;
     int p_kv = 0, p_npages = 0, p_off = 0, p_nmain = 0, p_kind = 0;
     int pid_base = 0, pid_cur = 0, pid_next = 0;
+    int q_ahead = -1;   // lane 0 of the producer: queue position reserved ~2 stages before it is needed
     auto issue_next = [&](int slot) {
         if (p_done) return;
         if (p_item < 0) {
@@ -202,7 +203,8 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8, KW_>::WARPS *
                 if (p_n == 0)   // the slot is ours once launch - kSchedSlots rewound it (rarely waits)
                     for (unsigned ns = 64; ld_acquire_gpu(sched + 3) != p.launch; ns = min(ns * 2, 1024u))
                         __nanosleep(ns);
-                qi = atomicAdd(sched, 1);
+                qi = q_ahead >= 0 ? q_ahead : atomicAdd(sched, 1);
+                q_ahead = -1;
             }
             qi = __shfl_sync(0xffffffffu, qi, 0);
             const bool live_q = qi < n_items;
@@ -274,6 +276,10 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8, KW_>::WARPS *
         }
         __syncwarp();
         if (++p_st * PPS >= p_npages) p_item = -1;
+        // reserve the next queue position two stages before this item runs out of stages to
+        // issue: the atomic's round trip then overlaps this warp's compute instead of sitting
+        // between items (a full item ahead would freeze the dynamic balance: measured 1.5x slower)
+        if (lane == 0 && p_item >= 0 && q_ahead < 0 && (p_st + 2) * PPS >= p_npages) q_ahead = atomicAdd(sched, 1);
     };
     if (producer) {
         for (int s = 0; s < C::NS; ++s) issue_next(s);
