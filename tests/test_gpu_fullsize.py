@@ -70,3 +70,54 @@ def test_qwen_config_full_size_sampled_fp8_pages():
 def test_gemma_config_full_size_sampled_fp8_pages():
     eo, el = _run("gemma", 6, {0, 40}, [0, 5], fp8=True)
     assert eo <= 2e-2 and el <= 1e-3, (eo, el)
+
+
+def test_long32k_config_full_size_sampled():
+    """BJ config 4: 128 agents at 30k-32k contexts + one fork each, up to 64 splits per range,
+    the 64-call model step over 4 resident layers (bench.py's launch configuration)."""
+    eo, el = _run("long", 4, {0, 77, 127}, [0, 33, 63])
+    assert eo <= 2e-2 and el <= 1e-3, (eo, el)
+
+
+def test_extend_mixed_step_full_size_sampled():
+    """F2 at BJ config 1's size on the tcgen05 path (bench_extend.py's launch configuration:
+    max_rows 128, folded tails, 8 resident layers PDL-chained): every parent decodes one token
+    while its fork prefills its 16-token prompt; sampled groups vs the fp64 extend oracle."""
+    from oracle.attention import extend_attention
+    from oracle.replay import bits_to_f64
+    from spa_inputs import workloads
+
+    rec = workloads.qwen()
+    m = rec.model
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    Lr = 4
+    layers = list(range(Lr))
+    pool = spa.Pool(Lr, m.num_q_heads, m.num_kv_heads, m.head_dim, bench.pages_for(rec, 4), device=dev)
+    ids, reqs, batch = bench.build_batch(spa, pool, rec, layers, slice(0, m.num_kv_heads), dev)
+    lens = [pool.page_table(r)[2] for r in reqs]
+    nq = [1 if who == "main" else min(16, n) for (gi, who), n in zip(batch, lens)]
+    rows = int(sum(nq))
+    q = kv_bits_torch(rec.seed, KIND_Q, 3_000_000, layers, np.arange(rows), m.num_q_heads, m.head_dim, dev)
+    o = torch.empty((Lr, rows, m.num_q_heads, m.head_dim), dtype=torch.bfloat16, device=dev)
+    lse = torch.empty((Lr, rows, m.num_q_heads), dtype=torch.float32, device=dev)
+    plan = spa.Plan(pool, max_rows=128)
+    plan.plan(reqs, 0, stream=stream, n_query=nq)
+    for i in range(2 * Lr):   # repeated launches of one plan
+        plan.decode(i % Lr, q[i % Lr].contiguous(), o[i % Lr], lse[i % Lr], scale=m.softmax_scale, stream=stream)
+    torch.cuda.synchronize()
+    starts = np.concatenate([[0], np.cumsum(nq)])
+    worst = [0.0, 0.0]
+    for li in (0, Lr - 1):
+        qb = kv_bits_np(rec.seed, KIND_Q, 3_000_000, [li], np.arange(rows), m.num_q_heads, m.head_dim)[0]
+        for i, (gi, who) in enumerate(batch):
+            if gi not in (0, 17, 31):
+                continue
+            K = bits_to_f64(bench.logical_kv_np(rec, gi, who, [li], KIND_K)[0])
+            V = bits_to_f64(bench.logical_kv_np(rec, gi, who, [li], KIND_V)[0])
+            r0, r1 = int(starts[i]), int(starts[i + 1])
+            O, L = extend_attention(bits_to_f64(qb[r0:r1]), K, V, m.softmax_scale)
+            worst[0] = max(worst[0], float(np.abs(o[li, r0:r1].float().cpu().numpy() - O).max()))
+            worst[1] = max(worst[1], float(np.abs(lse[li, r0:r1].cpu().numpy() - L).max()))
+    assert worst[0] <= 2e-2 and worst[1] <= 1e-3, worst
