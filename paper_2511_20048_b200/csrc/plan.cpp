@@ -57,17 +57,24 @@ extern "C" {
 
 // Kernel geometry of a plan with `mt` 16-row tiles per item: teams per CTA and key-split
 // warps per row tile.  32-row items take one warp per row tile over every page of a stage
-// (kw 1, 4 teams: measured 1.4x the key-split layout at k = 3, profiles/r02_*); fp8 pools
-// keep the key-split layout (the only fp8 instantiation).
+// (kw 1, 4 teams: measured 1.4x the key-split layout at k = 3, profiles/r02_*).  fp8 pools
+// take kw 1 for 16-row items too: 8 one-warp teams (each warp its own ring and producer: no
+// partner to wait for at every stage, no column-half exchange at item end) measured 93 ->
+// 80 us per layer on BJ config 1 (profiles/r02_fp8_kw1.txt); bf16 16-row items keep the
+// key-split pairs (one-warp teams fit only one bf16 page per stage: 113 vs 112 us, Gemma
+// local 116 vs 103 us).  An explicit teams_per_cta the kw-1 layout does not support keeps kw 2.
 static spa_status set_geometry(spa_plan* P, int mt, int teams_req) {
     P->mt = mt;
+    const bool fp8 = P->pool->kv_fp8;
     int teams = teams_req;
     if (const char* e = std::getenv("SPA_TEAMS")) teams = std::atoi(e);
-    int kw = mt == 2 && !P->pool->kv_fp8 ? 1 : 2;
-    if (const char* e = std::getenv("SPA_KW")) kw = std::atoi(e) == 1 && mt == 2 && !P->pool->kv_fp8 ? 1 : 2;
-    if (teams == 0) teams = kw == 1 ? 4 : mt == 1 ? 4 : mt == 2 ? 2 : 1;
+    int kw = mt == 2 || (fp8 && mt == 1) ? 1 : 2;
+    if (const char* e = std::getenv("SPA_KW")) kw = std::atoi(e) == 1 && mt <= 2 ? 1 : 2;
+    if (teams == 0) teams = kw == 1 ? (mt == 1 ? 8 : 4) : mt == 1 ? 4 : mt == 2 ? 2 : 1;
+    else if (kw == 1 && !decode_teams_supported(mt, teams, 1)) kw = 2;
     if (!decode_teams_supported(mt, teams, kw))
-        return fail(SPA_ERR_UNSUPPORTED, "teams_per_cta must be 1, 2 or 4 (4 only with max_rows 16 or 32, 1 with 64)");
+        return fail(SPA_ERR_UNSUPPORTED,
+                    "teams_per_cta must be 1, 2 or 4 (4 only with max_rows 16 or 32, 1 with 64; 8 with one-warp teams)");
     P->teams = teams;
     P->kw = kw;
     P->n_teams = P->num_ctas * teams;
