@@ -184,8 +184,9 @@ typedef struct spa_plan_config {
                                4 (default for max_rows 16): 4 x 3-stage rings; 2: 2 x 6; 1: 1 x 12
                                (deeper rings stream faster per item: small batches).  32-row
                                items use 4 teams of 2 warps (one per 16-row tile, each taking
-                               every page of a stage; fp8 pools: 2 teams of 4).  Must be 0 with
-                               max_rows 0.                                                       */
+                               every page of a stage).  fp8 pools, 16-row items: 0 selects 8
+                               one-warp teams (each warp its own 3-stage ring of 2 pages);
+                               1, 2 or 4 keep the key-split pairs.  Must be 0 with max_rows 0. */
 } spa_plan_config;
 
 /* cfg may be NULL (defaults).  The plan keeps a pointer to `pool`. */
