@@ -395,7 +395,9 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
             pages_all += np;
             if (int64_t(c.members.size()) * G > 16) pages_big += np;
         }
-        const int mt = G > 16 || (!pool->kv_fp8 && pages_big * 10 > pages_all * 3) ? 2 : 1;
+        // (fp8 pools too since the one-warp-per-tile 32-row fp8 kernel: sweep B = 256, f = 0.75
+        //  253 vs 266 us with 16-row items; profiles/r02_fp8_rows.txt)
+        const int mt = G > 16 || pages_big * 10 > pages_all * 3 ? 2 : 1;
         if (mt != P->mt)
             if (spa_status st = set_geometry(P, mt, 0)) return st;
     }
