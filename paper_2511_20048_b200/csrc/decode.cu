@@ -302,6 +302,59 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8, KW_>::WARPS *
         }
         pend_nm = 0;
     };
+    // per-row state of the current item (row_setup fills it from global memory)
+    int lo0 = 0, lo1 = 0, hi0 = INT_MAX, hi1 = INT_MAX;
+    // folded tails (reading #21): item pages [tk, tk + tn) are the row's own, from token tt
+    int tk0 = 0, tn0 = 0, tt0 = 0, tk1 = 0, tn1 = 0, tt1 = 0;
+    uint32_t qa[KS][4];   // query A fragments (raw bf16 pairs until the F8 conversion)
+    auto row_setup = [&](const TeamItem& d) {
+        const int Rn = d.n_members * G;
+        const int r0 = wt * 16 + (lane >> 2), r1 = r0 + 8;
+        lo0 = lo1 = 0;
+        hi0 = hi1 = INT_MAX;
+        tk0 = tn0 = tt0 = tk1 = tn1 = tt1 = 0;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) qa[ks][0] = qa[ks][1] = qa[ks][2] = qa[ks][3] = 0u;
+        if (wt * 16 >= Rn) return;
+        const __nv_bfloat16* q0 = nullptr;
+        const __nv_bfloat16* q1 = nullptr;
+        if (r0 < Rn) {
+            const int mb = r0 / G;
+            const Member m = mems[d.member_off + mb];
+            lo0 = m.lo;
+            hi0 = m.hi;
+            tk0 = m.tail_k0;
+            tn0 = m.tail_n;
+            tt0 = m.tail_tok;
+            q0 = p.q + m.row * p.q_sr + (d.kv_head * G + r0 - mb * G) * p.q_sh;
+        }
+        if (r1 < Rn) {
+            const int mb = r1 / G;
+            const Member m = mems[d.member_off + mb];
+            lo1 = m.lo;
+            hi1 = m.hi;
+            tk1 = m.tail_k0;
+            tn1 = m.tail_n;
+            tt1 = m.tail_tok;
+            q1 = p.q + m.row * p.q_sr + (d.kv_head * G + r1 - mb * G) * p.q_sh;
+        }
+        // fp8: the MMA's k index 2t+i (+8) reads channel 4t+i (+2) of each 16-channel block
+        // -- the same permutation as the K fragment, so q.k is unchanged -- (f16 after the
+        // conversion at item start)
+        const int cq = F8 ? 4 * (lane & 3) : 2 * (lane & 3);
+        const int c2 = F8 ? 2 : 8;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+            if (q0) {
+                qa[ks][0] = *reinterpret_cast<const uint32_t*>(q0 + ks * 16 + cq);
+                qa[ks][2] = *reinterpret_cast<const uint32_t*>(q0 + ks * 16 + cq + c2);
+            }
+            if (q1) {
+                qa[ks][1] = *reinterpret_cast<const uint32_t*>(q1 + ks * 16 + cq);
+                qa[ks][3] = *reinterpret_cast<const uint32_t*>(q1 + ks * 16 + cq + c2);
+            }
+        }
+    };
     while (true) {
         // the first stage of the next item (or the end-of-queue marker) has landed
         mbar_wait(full_bar(slot), phase);
@@ -322,55 +375,14 @@ __global__ void __launch_bounds__(DecodeCfg<D, MT, PPS, TEAMS, F8, KW_>::WARPS *
         const int row0 = wt * 16 + (lane >> 2), row1 = row0 + 8;
 
         // ---- per-row setup: member, window bound lo and causal bound hi (keys [lo, hi) are
-        //      live), query fragments (padding rows: q = 0, lo = 0, hi = INT_MAX)
-        int lo0 = 0, lo1 = 0, hi0 = INT_MAX, hi1 = INT_MAX;
-        // folded tails (reading #21): item pages [tk, tk + tn) are the row's own, from token tt
-        int tk0 = 0, tn0 = 0, tt0 = 0, tk1 = 0, tn1 = 0, tt1 = 0;
-        uint32_t qa[KS][4];
+        //      live), query fragments (padding rows: q = 0, lo = 0, hi = INT_MAX).  (Loading
+        //      them during the previous item's last stage instead measured 1-3 % slower.)
+        row_setup(dsc);
+        if (F8 && active)
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) qa[ks][0] = qa[ks][1] = qa[ks][2] = qa[ks][3] = 0u;
-        if (active) {
-            const __nv_bfloat16* q0 = nullptr;
-            const __nv_bfloat16* q1 = nullptr;
-            if (row0 < R) {
-                const int mb = row0 / G;
-                const Member m = mems[dsc.member_off + mb];
-                lo0 = m.lo;
-                hi0 = m.hi;
-                tk0 = m.tail_k0;
-                tn0 = m.tail_n;
-                tt0 = m.tail_tok;
-                q0 = p.q + m.row * p.q_sr + (itm.kv_head * G + row0 - mb * G) * p.q_sh;
-            }
-            if (row1 < R) {
-                const int mb = row1 / G;
-                const Member m = mems[dsc.member_off + mb];
-                lo1 = m.lo;
-                hi1 = m.hi;
-                tk1 = m.tail_k0;
-                tn1 = m.tail_n;
-                tt1 = m.tail_tok;
-                q1 = p.q + m.row * p.q_sr + (itm.kv_head * G + row1 - mb * G) * p.q_sh;
-            }
-            // fp8: the MMA's k index 2t+i (+8) reads channel 4t+i (+2) of each 16-channel block
-            // -- the same permutation as the K fragment, so q.k is unchanged -- in f16
-            const int cq = F8 ? 4 * (lane & 3) : 2 * (lane & 3);
-            const int c2 = F8 ? 2 : 8;
+            for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
-            for (int ks = 0; ks < KS; ++ks) {
-                if (q0) {
-                    qa[ks][0] = *reinterpret_cast<const uint32_t*>(q0 + ks * 16 + cq);
-                    qa[ks][2] = *reinterpret_cast<const uint32_t*>(q0 + ks * 16 + cq + c2);
-                }
-                if (q1) {
-                    qa[ks][1] = *reinterpret_cast<const uint32_t*>(q1 + ks * 16 + cq);
-                    qa[ks][3] = *reinterpret_cast<const uint32_t*>(q1 + ks * 16 + cq + c2);
-                }
-                if (F8)
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) qa[ks][e] = bf16x2_to_f16x2(qa[ks][e]);
-            }
-        }
+                for (int e = 0; e < 4; ++e) qa[ks][e] = bf16x2_to_f16x2(qa[ks][e]);
         if (trace) {   // timeline: the row setup's loads have landed
             uint32_t d0 = qa[0][0] | qa[KS - 1][3] | uint32_t(lo0) | uint32_t(tk1);
             asm volatile("mov.b32 %0, %0;" : "+r"(d0));
