@@ -427,6 +427,12 @@ class Plan:
             return [flat[i:i + w.value] for i in range(0, len(flat), w.value)]
         return flat
 
+    def geometry(self) -> tuple:
+        """(num_ctas, teams_per_cta, warps_per_cta) of the plan's decode launches."""
+        nc, tm, wp = c_int32(), c_int32(), c_int32()
+        _check(lib().spa_debug_plan_geometry(self.h, ctypes.byref(nc), ctypes.byref(tm), ctypes.byref(wp)))
+        return nc.value, tm.value, wp.value
+
     def num_ctas_hint(self) -> int:
         nc, tm, wp = c_int32(), c_int32(), c_int32()
         _check(lib().spa_debug_plan_geometry(self.h, ctypes.byref(nc), ctypes.byref(tm), ctypes.byref(wp)))
