@@ -9,9 +9,13 @@ import sys
 
 
 def load(path):
+    """The first kernel's source table (a capture of several launches repeats the table,
+    each behind its own "Kernel Name" line)."""
     f = io.TextIOWrapper(gzip.open(path)) if path.endswith(".gz") else open(path)
     rows = list(csv.reader(f))
-    return rows[1], rows[2:]
+    ends = [i for i, r in enumerate(rows) if i > 0 and r and r[0] == "Kernel Name"]
+    rows = rows[:ends[0]] if ends else rows
+    return rows[1], [r for r in rows[2:] if len(r) == len(rows[1])]
 
 
 def main():
