@@ -685,10 +685,14 @@ def run_spa(args):
     if rank == 0:
         cpu = cpu_baseline(recipe, batch, args.cpu_seconds) if world == 1 and not args.profile else None
         ck = clocks.summary(local)
-        sep = args.merge_mode == 2
+        # merge_mode 0 on fp8 pools decoded by one-warp teams (teams == warps per CTA) without
+        # the fused gather also launches merge_kernel (include/spa.h merge_mode)
+        _, g_teams, g_warps = next(iter(plans.values())).geometry()
+        sep = args.merge_mode == 2 or (args.merge_mode == 0 and fp8 and g_teams == g_warps and peer is None)
         launches_per_step = (-(-N // 896)) + sum(
             1 + (1 if sep and per_window[w]["stats"]["n_records"] > 0 else 0) for _, w in sched)
-        kname = {0: "decode_kernel (split merge in-kernel, tail phase)",
+        kname = {0: "decode_kernel + merge_kernel (fp8 one-warp teams)" if sep else
+                 "decode_kernel (split merge in-kernel, tail phase)",
                  1: "decode_kernel (split merge in-kernel, last arriver)",
                  2: "decode_kernel + merge_kernel (one spa_decode_attention call)"}[args.merge_mode]
         result = {

@@ -175,8 +175,10 @@ typedef struct spa_plan_config {
     int32_t split_pages;    /* max pages per split; 0 = auto (balance over the persistent grid)  */
     int32_t num_ctas;       /* persistent grid size; 0 = number of SMs                            */
     int32_t merge_mode;     /* where split partials are merged (spa_merge_splits semantics always):
-                               0 (default): inside the decode kernel, by teams that found the work
-                                 queue empty (tail phase);
+                               0 (default): the library's choice -- inside the decode kernel, by
+                                 teams that found the work queue empty (tail phase); fp8 pools
+                                 decoded by one-warp teams (16-row items) without a peer
+                                 fan-out: by the merge_kernel launch of mode 2 (measured faster);
                                1: inside the decode kernel, by the last item of each (request, KV
                                  head) to finish;
                                2: by a separate merge_kernel launch (programmatic dependent launch) */

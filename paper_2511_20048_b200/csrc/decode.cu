@@ -913,6 +913,14 @@ bool decode_teams_supported(int mt, int teams, int kw) {
     return teams == 1 || teams == 2 || (teams == 4 && mt == 1);
 }
 
+// merge_mode 0 leaves the place of the split merge to the library: the kernel's tail phase,
+// except for fp8 pools decoded by one-warp teams without a peer fan-out, whose split records
+// are merged by the PDL-chained merge_kernel (BJ config 1 fp8: 75.9 vs 79.0 us per layer;
+// bf16 key-split teams keep the tail phase: 109.3 vs 112.3; profiles/r02_merge_modes.txt)
+bool merge_separately(const spa_plan* P, bool fan_out) {
+    return P->cfg.merge_mode == 0 && P->pool->kv_fp8 && P->kw == 1 && P->mt == 1 && !fan_out;
+}
+
 int launch_decode(const spa_plan* P, int32_t layer, const void* q, int64_t q_sr, int64_t q_sh, void* o, int64_t o_sr,
                   int64_t o_sh, float* lse, int64_t l_sr, int64_t l_sh, float scale, void* stream,
                   const PeerLaunch* peer) {
@@ -942,6 +950,7 @@ int launch_decode(const spa_plan* P, int32_t layer, const void* q, int64_t q_sr,
     dp.num_kv_heads = c.num_kv_heads;
     dp.group_size = c.num_q_heads / c.num_kv_heads;
     dp.fused_merge = P->cfg.merge_mode == 0 ? 2 : P->cfg.merge_mode == 1 ? 1 : 0;
+    if (merge_separately(P, peer && peer->world > 1)) dp.fused_merge = 0;
     dp.launch = int(P->launches++);
     dp.trace = P->trace;
     dp.trace_cap = P->trace_cap;

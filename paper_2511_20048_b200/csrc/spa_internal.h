@@ -210,6 +210,7 @@ int launch_merge_tasks(const spa_plan* P, void* o, int64_t o_sr, int64_t o_sh, f
 int launch_merge(int32_t n_req, int32_t num_heads, int32_t head_dim, const int32_t* rec_ptr, const float* part_o,
                  const float* part_lse, void* o, int64_t o_sr, int64_t o_sh, float* lse, int64_t l_sr, int64_t l_sh,
                  int grid_hint, void* stream);
+bool merge_separately(const spa_plan* P, bool fan_out);   // decode.cu: merge_mode 0 -> merge_kernel
 bool decode_teams_supported(int mt, int teams, int kw);   // decode.cu: compiled (row tiles, teams/CTA, key split)
 // ext.cu: the tcgen05 kernel for 128-row (extend) plans
 bool ext_supported(int head_dim);
