@@ -99,12 +99,12 @@ def fp8_scales(inputs: families.BatchInputs) -> np.ndarray:
 
 
 def run_parity(recipe, family="flat", window=0, sharing=True, max_rows=16, split_pages=0, num_ctas=0,
-               layers=None, pre_shuffle=0, merge_mode=0, fp8=False):
+               layers=None, pre_shuffle=0, merge_mode=0, fp8=False, teams_per_cta=0):
     inp = families.make_inputs(recipe, family, layers=layers)
     scales = fp8_scales(inp) if fp8 else None
     gb = GpuBatch(inp, pre_shuffle=pre_shuffle, kv_scale=scales)
     plan = spa.Plan(gb.pool, sharing=sharing, max_rows=max_rows, split_pages=split_pages, num_ctas=num_ctas,
-                    merge_mode=merge_mode)
+                    merge_mode=merge_mode, teams_per_cta=teams_per_cta)
     plan.plan(gb.reqs, window)
     rp = Replay(inp, kv_fp8_scale=scales)
     errs = []

@@ -87,6 +87,26 @@ def test_fp8_plan_variants(sharing, merge_mode, split_pages, max_rows):
         assert eo <= O_TOL and el <= LSE_TOL, (eo, el)
 
 
+@pytest.mark.parametrize("max_rows,teams,merge_mode,geometry", [
+    (16, 0, 0, (8, 8)),    # 8 one-warp teams, split merge in merge_kernel (merge_mode 0's choice)
+    (16, 0, 1, (8, 8)),    # one-warp teams, last-arriver merge in the kernel
+    (16, 4, 0, (4, 8)),    # key-split pairs (explicit teams_per_cta), tail-phase merge
+    (16, 2, 1, (2, 4)),
+    (16, 1, 0, (1, 2)),
+    (32, 0, 0, (4, 8)),    # one warp per 16-row tile, 4 teams
+])
+def test_fp8_team_geometries(max_rows, teams, merge_mode, geometry):
+    """Every fp8 decode instantiation (one-warp teams and key-split pairs) against the oracle,
+    with forced splits so the split merge runs (S5 "Team geometry")."""
+    rec = workloads.random_small(37, _model(), max_prefix=600)
+    errs, _, _, plan, _ = run_parity(rec, "needle_shared_pos", split_pages=3, max_rows=max_rows, merge_mode=merge_mode,
+                                     fp8=True, teams_per_cta=teams)
+    assert plan.geometry()[1:] == geometry
+    assert plan.stats()["n_records"] > 0
+    for eo, el in errs:
+        assert eo <= O_TOL and el <= LSE_TOL, (eo, el)
+
+
 def test_fp8_sliding_window_and_decode_steps():
     rec = workloads.random_small(33, _model(1), max_prefix=700)
     inp = families.make_inputs(rec, "needle_tail_pos")
