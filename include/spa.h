@@ -187,8 +187,9 @@ typedef struct spa_plan_config {
                                (deeper rings stream faster per item: small batches).  32-row
                                items use 4 teams of 2 warps (one per 16-row tile, each taking
                                every page of a stage).  fp8 pools, 16-row items: 0 selects 8
-                               one-warp teams (each warp its own 3-stage ring of 2 pages);
-                               1, 2 or 4 keep the key-split pairs.  Must be 0 with max_rows 0. */
+                               one-warp teams (each warp its own 3-stage ring of 2 pages), 12
+                               (2-stage rings) for windowed plans; 1, 2 or 4 keep the
+                               key-split pairs.  Must be 0 with max_rows 0.                      */
 } spa_plan_config;
 
 /* cfg may be NULL (defaults).  The plan keeps a pointer to `pool`. */

@@ -98,7 +98,8 @@ struct DecodeCfg {
     static constexpr int OFF_TQ = OFF_SLOT + TEAMS * 4;
     static constexpr int OFF_COMB = (OFF_TQ + TEAMS * QN * 32 + 15) & ~15;
     static constexpr int SMEM = 1024 + OFF_COMB + COMB_BYTES;
-    static_assert(NS >= 2 && (TEAMS < 4 || NS >= 3), "pipeline needs >= 2 stages (3 with 4 teams)");
+    static_assert(NS >= 2 && (TEAMS < 4 || NS >= 3 || (KW == 1 && TEAMS > 8)),
+                  "pipeline needs >= 2 stages (3 with 4 key-split teams; 12 one-warp teams: 2)");
     static_assert(PPS % KW == 0, "each key-split warp takes whole pages");
     static_assert(KW == 1 || KW == 2, "one or two key-split warps per row tile");
     static_assert(OFF_COMB - OFF_BARS <= MISC_BYTES, "misc shared-memory region too small");
@@ -874,7 +875,8 @@ static int launch_decode_t(const spa_plan* P, const DecodeParams& dp, void* stre
 #endif
 static int launch_decode_f8(const spa_plan* P, const DecodeParams& dp, void* stream) {
     constexpr int S = SPA_F8_PPS;
-    if (P->kw == 1) {   // one warp per 16-row tile: 8 one-warp teams (16 rows), 4 teams of 2 (32 rows)
+    if (P->kw == 1) {   // one warp per 16-row tile: 8 or 12 one-warp teams (16 rows), 4 teams of 2 (32 rows)
+        if (P->mt == 1 && P->teams == 12) return launch_decode_t<128, 1, 2, 12, true, 1>(P, dp, stream);
         if (P->mt == 1) return launch_decode_t<128, 1, 2, 8, true, 1>(P, dp, stream);
         return launch_decode_t<128, 2, S, 4, true, 1>(P, dp, stream);
     }
@@ -896,7 +898,9 @@ static int launch_decode_d(const spa_plan* P, const DecodeParams& dp, void* stre
     // 32-row items, one warp per row tile over every page of a stage (no key split): 4 teams
     if (P->mt == 2 && P->kw == 1) return launch_decode_t<D, 2, 2, 4, false, 1>(P, dp, stream);
     // 16-row items, one-warp teams (8 per CTA, one page per stage)
-    if (P->mt == 1 && P->kw == 1) return launch_decode_t<D, 1, SPA_KW1_PPS, 8, false, 1>(P, dp, stream);
+    if (P->mt == 1 && P->kw == 1)
+        return P->teams == 8 ? launch_decode_t<D, 1, SPA_KW1_PPS, 8, false, 1>(P, dp, stream)
+                             : int(cudaErrorNotSupported);
     if (P->mt == 1) {
         if (P->teams == 1) return launch_decode_t<D, 1, 2, 1>(P, dp, stream);
         if (P->teams == 2) return launch_decode_t<D, 1, 2, 2>(P, dp, stream);
@@ -908,7 +912,7 @@ static int launch_decode_d(const spa_plan* P, const DecodeParams& dp, void* stre
 }
 
 bool decode_teams_supported(int mt, int teams, int kw) {
-    if (kw == 1) return (mt == 2 && teams == 4) || (mt == 1 && teams == 8);
+    if (kw == 1) return (mt == 2 && teams == 4) || (mt == 1 && (teams == 8 || teams == 12));
     if (mt == 4 || mt == 8) return teams == 1;
     return teams == 1 || teams == 2 || (teams == 4 && mt == 1);
 }

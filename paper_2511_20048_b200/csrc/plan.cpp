@@ -68,6 +68,7 @@ static spa_status set_geometry(spa_plan* P, int mt, int teams_req) {
     const bool fp8 = P->pool->kv_fp8;
     int teams = teams_req;
     if (const char* e = std::getenv("SPA_TEAMS")) teams = std::atoi(e);
+    P->teams_auto = teams == 0;
     int kw = mt == 2 || (fp8 && mt == 1) ? 1 : 2;
     if (const char* e = std::getenv("SPA_KW")) kw = std::atoi(e) == 1 && mt <= 2 ? 1 : 2;
     if (teams == 0) teams = kw == 1 ? (mt == 1 ? 8 : 4) : mt == 1 ? 4 : mt == 2 ? 2 : 1;
@@ -400,6 +401,14 @@ spa_status plan_rows(spa_plan* P, const std::vector<VRow>& V, int32_t window, vo
         const int mt = G > 16 || pages_big * 10 > pages_all * 3 ? 2 : 1;
         if (mt != P->mt)
             if (spa_status st = set_geometry(P, mt, 0)) return st;
+    }
+    // fp8 one-warp teams: 12 per CTA (2-stage rings) for windowed plans, whose items are at
+    // most a window long -- more warps hide the per-item setup and drain (Gemma-3 local
+    // layers 86 -> 78 us) -- and 8 (3-stage rings) otherwise (config 1: 79 vs 84 us with 12;
+    // profiles/r02_fp8_teams.txt)
+    if (P->pool->kv_fp8 && P->mt == 1 && P->kw == 1 && P->teams_auto) {
+        P->teams = window > 0 ? 12 : 8;
+        P->n_teams = P->num_ctas * P->teams;
     }
     const int max_members = std::max(1, P->mt * 16 / G);
     for (auto& c : classes) {

@@ -126,6 +126,7 @@ struct spa_plan {
     spa_plan_config cfg{};
     int mt = 1;                 // m16 tiles (warps) per team: max_rows / 16
     int teams = 4;              // teams (work-item streams with private rings) per CTA
+    bool teams_auto = true;     // teams chosen by the library (teams_per_cta 0, no SPA_TEAMS)
     int kw = 2;                 // key-split warps per row tile (1: a warp takes every page of a stage)
     bool auto_rows = false;     // max_rows 0: 16- or 32-row items chosen per batch (spa_decode_plan)
     int n_teams = 0;

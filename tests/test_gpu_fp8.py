@@ -107,6 +107,18 @@ def test_fp8_team_geometries(max_rows, teams, merge_mode, geometry):
         assert eo <= O_TOL and el <= LSE_TOL, (eo, el)
 
 
+@pytest.mark.parametrize("merge_mode", [0, 1])
+def test_fp8_windowed_twelve_teams(merge_mode):
+    """Windowed fp8 plans run 12 one-warp teams per CTA (2-stage rings); forced splits."""
+    rec = workloads.random_small(39, _model(), max_prefix=900)
+    errs, _, _, plan, _ = run_parity(rec, "needle_tail_pos", window=200, split_pages=3, merge_mode=merge_mode,
+                                     fp8=True)
+    assert plan.geometry()[1:] == (12, 12)
+    assert plan.stats()["n_records"] > 0
+    for eo, el in errs:
+        assert eo <= O_TOL and el <= LSE_TOL, (eo, el)
+
+
 def test_fp8_sliding_window_and_decode_steps():
     rec = workloads.random_small(33, _model(1), max_prefix=700)
     inp = families.make_inputs(rec, "needle_tail_pos")

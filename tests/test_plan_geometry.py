@@ -45,3 +45,21 @@ def test_fp8_auto_rows_takes_32_row_items_for_k3_forks():
     plan.plan([parent] + forks)
     assert plan.geometry()[1:] == (4, 8)       # 32-row items: 4 teams, one warp per row tile
     assert plan.stats()["rows_max"] == 20
+
+
+@pytest.mark.parametrize("fp8,window,teams_req,expect", [
+    (True, 0, 0, (8, 8)),       # fp8, full attention: 8 one-warp teams
+    (True, 256, 0, (12, 12)),   # fp8, windowed: 12 one-warp teams (2-stage rings)
+    (True, 256, 4, (4, 8)),     # explicit teams: key-split pairs
+    (False, 256, 0, (4, 8)),    # bf16 windowed: key-split pairs
+])
+def test_windowed_geometry(fp8, window, teams_req, expect):
+    pool = qwen_pool(fp8)
+    reqs = []
+    for n in (700, 1500):
+        r = pool.alloc()
+        pool.append([r], [n])
+        reqs.append(r)
+    plan = spa.Plan(pool, max_rows=16, teams_per_cta=teams_req, num_ctas=148)
+    plan.plan(reqs, window)
+    assert plan.geometry()[1:] == expect
